@@ -1,0 +1,106 @@
+/* lrq.h — C ABI of the B200-native LR-QAOA state-vector engine (liblrq.so).
+ *
+ * Drop-in boundary for the reference package lrqbench (pure Python/numpy,
+ * /root/reference/pkg/src/lrqbench).  Every entry point below replaces one
+ * reference interface; the Python mirror paper_2604_26423_b200 binds them
+ * with ctypes (see INTEGRATION.md for the binding a maintainer would add to
+ * the reference itself).
+ *
+ * Conventions
+ *   - plain C types only; host pointers unless a name says _dev;
+ *   - basis index z has qubit/vertex k at bit k (engine.py:3-4);
+ *   - edge arrays are in lexicographic (i<j) order, length n(n-1)/2
+ *     (problem.py:32-34);
+ *   - return codes mirror the reference exception taxonomy / CLI exit codes
+ *     (errors.py:8-26, cli.py:64-67): 0 ok, 2 ValidationError,
+ *     3 CapacityError, 4 StateError/AbortedRunError (runtime);
+ *     lrq_last_error() gives the message of the calling thread's last failure.
+ */
+#ifndef LRQ_H
+#define LRQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRQ_OK 0
+#define LRQ_EVALIDATION 2
+#define LRQ_ECAPACITY 3
+#define LRQ_ERUNTIME 4
+
+#define LRQ_ABI_VERSION 1
+
+typedef struct lrq_state lrq_state; /* one state vector (or one rank's shard) in HBM */
+
+typedef struct lrq_reduction {
+  double sum_p;        /* sum_z |a_z|^2 (float64)                          */
+  double sum_p_cut;    /* sum_z |a_z|^2 C(z)  -> exact r = sum_p_cut / C*  */
+  double min_energy;   /* min_z E_w(z) over z with top bit 0 (spin form)   */
+  uint64_t argmax_cut; /* lowest-index z attaining it (= argmax C)         */
+} lrq_reduction;
+
+/* library / device ------------------------------------------------------- */
+int lrq_abi_version(void);
+const char *lrq_last_error(void);
+int lrq_device_count(int *count);
+
+/* Host-only: JSON description of the sweep plan for (n, precision_bytes, p).
+ * No GPU needed; used by CPU tests of the planner.                          */
+int lrq_describe_plan(int num_qubits, int precision_bytes, int p, char *buf, size_t cap);
+
+/* state lifecycle — replaces engine.py:99-110 zero_state/check_memory.
+ * precision_bytes: 8 = complex64 (Precision.FP32), 16 = complex128 (FP64).
+ * memory_budget: bytes allowed for the state; 0 = device capacity.
+ * Over budget -> 3 with the reference's message shape (engine.py:67-74).   */
+int lrq_create(int num_qubits, int precision_bytes, int device, uint64_t memory_budget, lrq_state **out);
+int lrq_destroy(lrq_state *s);
+
+/* cost function for the fused final pass: edge weights w (lex order),
+ * replaces the WmcInstance consumed by exact_expected_r (engine.py:229-235). */
+int lrq_set_cost(lrq_state *s, const double *w);
+
+/* run_circuit (engine.py:198-207) for an H-layer + p x (RZZ*, RX^n) circuit:
+ *   phase[k*E + e] = sum of theta/2 over the layer-k RZZ gates on edge e,
+ *   mixer[k]       = theta/2 of the layer-k RX gates (same on every qubit).
+ * Starts from |0..0>, applies the H layer, the p layers, and (if a cost was
+ * set) the fused final pass.  Synchronous.                                  */
+int lrq_run(lrq_state *s, int p, const double *phase, const double *mixer);
+
+/* reductions of the last run (exact_expected_r numerator, engine.py:214-226;
+ * exhaustive max cut argmax, problem.py:174-211).                            */
+int lrq_reduce(lrq_state *s, lrq_reduction *out);
+
+/* read-only pass: recompute the reductions and the sampler CDF from the
+ * current state with the current cost (zero cost if none was set).         */
+int lrq_recompute(lrq_state *s);
+
+/* inverse-CDF sampling (engine.py:254-273) with caller-supplied uniforms
+ * (the reference draws them from Philox("shots", 0) on the host).           */
+int lrq_sample(lrq_state *s, const double *u, int64_t shots, uint64_t *idx_out);
+
+/* amplitudes [start, start+count) -> host, complex64/complex128 interleaved. */
+int lrq_copy_amps(lrq_state *s, uint64_t start, uint64_t count, void *host_out);
+
+/* bit-exact cut values (problem.py:139-149) on the device. z==NULL means the
+ * contiguous range [start, start+count).                                    */
+int lrq_cut_values(int num_qubits, const double *w, const uint64_t *z, uint64_t start, int64_t count,
+                   double *out, int device);
+
+/* exhaustive max cut (optimal_cut_bruteforce, problem.py:174-211) on the
+ * device: lowest-index argmax of C; value re-evaluated bit-exactly.         */
+int lrq_max_cut(int num_qubits, const double *w, int device, uint64_t *argmax, double *value);
+
+/* timing: per-launch device milliseconds of the last lrq_run (CUDA events on
+ * the engine stream), plus the engine stream handle for external events.   */
+int lrq_set_timing(lrq_state *s, int enable);
+int lrq_get_timings(lrq_state *s, double *ms, char *kinds, int cap, int *count);
+int lrq_stream(lrq_state *s, void **stream_out);
+int lrq_synchronize(lrq_state *s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRQ_H */

@@ -1,0 +1,54 @@
+"""B200-native LR-QAOA state-vector simulator (drop-in for lrqbench's hot path).
+
+The public names mirror lrqbench/__init__.py for the noiseless path
+(instance -> circuit -> run_circuit -> exact_expected_r / sample -> ratios).
+Compute runs in liblrq.so (hand-written sm_100a CUDA, C ABI in include/lrq.h);
+importing the package does not need a GPU, calling the engine does.
+"""
+
+__version__ = "0.1.0"
+
+from .circuit import (
+    CircuitIR,
+    GateOp,
+    LayerArrays,
+    LrQaoaParams,
+    Schedule,
+    build_circuit,
+    build_schedule,
+    gate_counts,
+    lower_circuit,
+)
+from .engine import (
+    Precision,
+    ShotSet,
+    StateVector,
+    check_memory,
+    exact_expected_r,
+    run_circuit,
+    sample,
+    save_statevector,
+    state_bytes,
+    uniform_amplitude,
+)
+from .errors import AbortedRunError, CapacityError, FitError, StateError, ValidationError
+from .problem import (
+    OptimalCut,
+    WmcInstance,
+    approximation_ratio,
+    as_index,
+    bitstring_to_index,
+    complete_edge_list,
+    cut_value,
+    cut_values,
+    cut_values_range,
+    generate_instance,
+    index_to_bitstring,
+    load_instance,
+    optimal_cut_bruteforce,
+    random_baseline_expectation,
+    save_instance,
+    shot_ratios,
+    solve_instance,
+)
+from .rng import derive_rng, derive_seed

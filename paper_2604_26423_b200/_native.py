@@ -1,0 +1,212 @@
+"""ctypes binding of liblrq.so (include/lrq.h).
+
+The engine has no CPU path: if the library is missing or no CUDA device is
+visible, every compute entry point raises.  Return codes map onto the
+reference's exception taxonomy (lrqbench errors.py:8-26): 2 -> ValidationError,
+3 -> CapacityError, 4 -> StateError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import CapacityError, StateError, ValidationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "liblrq.so")
+ABI_VERSION = 1
+
+_lib = None
+_lock = threading.Lock()
+
+_c_int, _c_i64, _c_u64, _c_dbl = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+_p = ctypes.c_void_p
+_state_p = ctypes.c_void_p
+
+
+class Reduction(ctypes.Structure):
+    _fields_ = [("sum_p", ctypes.c_double), ("sum_p_cut", ctypes.c_double),
+                ("min_energy", ctypes.c_double), ("argmax_cut", ctypes.c_uint64)]
+
+
+_SIGNATURES = {
+    "lrq_abi_version": ([], _c_int),
+    "lrq_last_error": ([], ctypes.c_char_p),
+    "lrq_device_count": ([ctypes.POINTER(_c_int)], _c_int),
+    "lrq_describe_plan": ([_c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
+    "lrq_create": ([_c_int, _c_int, _c_int, _c_u64, ctypes.POINTER(_state_p)], _c_int),
+    "lrq_destroy": ([_state_p], _c_int),
+    "lrq_set_cost": ([_state_p, _p], _c_int),
+    "lrq_run": ([_state_p, _c_int, _p, _p], _c_int),
+    "lrq_reduce": ([_state_p, ctypes.POINTER(Reduction)], _c_int),
+    "lrq_recompute": ([_state_p], _c_int),
+    "lrq_sample": ([_state_p, _p, _c_i64, _p], _c_int),
+    "lrq_copy_amps": ([_state_p, _c_u64, _c_u64, _p], _c_int),
+    "lrq_cut_values": ([_c_int, _p, _p, _c_u64, _c_i64, _p, _c_int], _c_int),
+    "lrq_max_cut": ([_c_int, _p, _c_int, ctypes.POINTER(_c_u64), ctypes.POINTER(_c_dbl)], _c_int),
+    "lrq_set_timing": ([_state_p, _c_int], _c_int),
+    "lrq_get_timings": ([_state_p, _p, ctypes.c_char_p, _c_int, ctypes.POINTER(_c_int)], _c_int),
+    "lrq_stream": ([_state_p, ctypes.POINTER(_p)], _c_int),
+    "lrq_synchronize": ([_state_p], _c_int),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+def lib():
+    """Load liblrq.so once; raise loudly if it has not been built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build the CUDA engine with "
+                    "`python -m paper_2604_26423_b200.build` (there is no CPU fallback)")
+            h = ctypes.CDLL(LIB_PATH)
+            for name, (args, res) in _SIGNATURES.items():
+                fn = getattr(h, name)
+                fn.argtypes = args
+                fn.restype = res
+            if h.lrq_abi_version() != ABI_VERSION:
+                raise RuntimeError("liblrq.so ABI version mismatch; rebuild the engine")
+            _lib = h
+        return _lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (lib().lrq_last_error() or b"").decode(errors="replace")
+    if rc == 2:
+        raise ValidationError(msg)
+    if rc == 3:
+        raise CapacityError(msg)
+    raise StateError(msg)
+
+
+def device_count() -> int:
+    c = _c_int(0)
+    rc = lib().lrq_device_count(ctypes.byref(c))
+    return int(c.value) if rc == 0 else 0
+
+
+def default_device() -> int:
+    """Device for new states: $LRQ_DEVICE, else 0 (one process per GPU; torchrun
+    launches pin CUDA_VISIBLE_DEVICES or pass LOCAL_RANK explicitly)."""
+    return int(os.environ.get("LRQ_DEVICE", "0"))
+
+
+def describe_plan(n: int, precision_bytes: int, p: int) -> str:
+    buf = ctypes.create_string_buffer(1 << 20)
+    check(lib().lrq_describe_plan(n, precision_bytes, p, buf, len(buf)))
+    return buf.value.decode()
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class DeviceState:
+    """Owning handle of one lrq_state (a state vector in HBM)."""
+
+    def __init__(self, n: int, precision_bytes: int, device: int | None = None, budget: int = 0):
+        self._h = None
+        self.n = n
+        self.precision_bytes = precision_bytes
+        self.device = default_device() if device is None else int(device)
+        h = _state_p()
+        check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise StateError("device state has been released")
+        return self._h
+
+    def close(self) -> None:
+        if self._h is not None and _lib is not None:
+            _lib.lrq_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- engine calls ---------------------------------------------------------
+    def set_cost(self, w: np.ndarray) -> None:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        check(lib().lrq_set_cost(self.handle, ptr(w)))
+
+    def run(self, phase: np.ndarray, mixer: np.ndarray) -> None:
+        phase = np.ascontiguousarray(phase, dtype=np.float64)
+        mixer = np.ascontiguousarray(mixer, dtype=np.float64)
+        check(lib().lrq_run(self.handle, int(mixer.size), ptr(phase), ptr(mixer)))
+
+    def reduce(self) -> Reduction:
+        r = Reduction()
+        check(lib().lrq_reduce(self.handle, ctypes.byref(r)))
+        return r
+
+    def recompute(self) -> None:
+        check(lib().lrq_recompute(self.handle))
+
+    def sample(self, u: np.ndarray) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.empty(u.size, dtype=np.uint64)
+        check(lib().lrq_sample(self.handle, ptr(u), u.size, ptr(out)))
+        return out
+
+    def copy_amps(self, start: int = 0, count: int | None = None) -> np.ndarray:
+        if count is None:
+            count = (1 << self.n) - start
+        dt = np.complex64 if self.precision_bytes == 8 else np.complex128
+        out = np.empty(count, dtype=dt)
+        check(lib().lrq_copy_amps(self.handle, start, count, ptr(out)))
+        return out
+
+    def set_timing(self, on: bool) -> None:
+        check(lib().lrq_set_timing(self.handle, 1 if on else 0))
+
+    def timings(self):
+        cnt = _c_int(0)
+        check(lib().lrq_get_timings(self.handle, None, None, 0, ctypes.byref(cnt)))
+        ms = np.zeros(max(1, cnt.value))
+        kinds = ctypes.create_string_buffer(max(1, cnt.value) + 1)
+        check(lib().lrq_get_timings(self.handle, ptr(ms), kinds, cnt.value, ctypes.byref(cnt)))
+        return list(ms[: cnt.value]), kinds.raw[: cnt.value].decode()
+
+    def stream(self) -> int:
+        s = _p()
+        check(lib().lrq_stream(self.handle, ctypes.byref(s)))
+        return int(s.value or 0)
+
+    def synchronize(self) -> None:
+        check(lib().lrq_synchronize(self.handle))
+
+
+def cut_values(n: int, w: np.ndarray, z: np.ndarray | None = None, start: int = 0, count: int = 0,
+               device: int | None = None) -> np.ndarray:
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    dev = default_device() if device is None else device
+    if z is not None:
+        z = np.ascontiguousarray(z, dtype=np.uint64)
+        count = z.size
+    out = np.empty(count, dtype=np.float64)
+    if count:
+        check(lib().lrq_cut_values(n, ptr(w), ptr(z) if z is not None else None, start, count, ptr(out), dev))
+    return out
+
+
+def max_cut(n: int, w: np.ndarray, device: int | None = None):
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    dev = default_device() if device is None else device
+    z = _c_u64(0)
+    v = _c_dbl(0.0)
+    check(lib().lrq_max_cut(n, ptr(w), dev, ctypes.byref(z), ctypes.byref(v)))
+    return int(z.value), float(v.value)

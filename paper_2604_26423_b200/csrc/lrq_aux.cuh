@@ -1,0 +1,269 @@
+// Auxiliary kernels: whole-state path for tiny n, deterministic finalisation
+// of the per-tile reductions (+ CDF block prefix), the two-level inverse-CDF
+// sampler, and the bit-exact sequential cut diagonal.
+#pragma once
+#include "lrq_device.cuh"
+
+namespace lrq {
+
+// ---------------------------------------------------------------------------
+// n < K: the whole circuit in one CTA, state in shared memory.
+// Same operations as the sweep path (phase exp(-i E_J), RX butterflies),
+// written plainly: tiny n is a correctness path, not a performance one.
+struct SmallParams {
+  void* amps;
+  int n, p;
+  const double* J;    // p * n * n
+  const double* mix;  // p * 2: (cos h, -sin h) of RX(theta), h = theta / 2
+  const double* W;    // n * n cost matrix (may be null: no reduction)
+  double init_re, init_im;
+  int load;  // start from the stored state instead of the init value
+  int min_bit;
+  double* red_p;
+  double* red_pE;
+  double* red_minE;
+  unsigned long long* red_arg;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
+  typedef typename CxT<T>::V V;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = P.n, N = 1 << n;
+  V* s = reinterpret_cast<V*>(smem);
+  double* red = reinterpret_cast<double*>(s + N);  // 8 warps * 4
+  const int t = threadIdx.x;
+  const V* g0 = reinterpret_cast<const V*>(P.amps);
+  for (int z = t; z < N; z += blockDim.x) {
+    if (P.load) {
+      s[z] = g0[z];
+    } else {
+      s[z].x = (T)P.init_re;
+      s[z].y = (T)P.init_im;
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < P.p; ++k) {
+    const double* J = P.J + (size_t)k * n * n;
+    for (int z = t; z < N; z += blockDim.x) {
+      double e = 0.0;
+      for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) e += J[i * n + j] * spin(z, i) * spin(z, j);
+      s[z] = cmul_amp(s[z], expmi(e));
+    }
+    __syncthreads();
+    const T c = (T)P.mix[2 * k], sn = (T)P.mix[2 * k + 1];
+    for (int q = 0; q < n; ++q) {
+      for (int pi = t; pi < N / 2; pi += blockDim.x) {
+        const int lo = ((pi >> q) << (q + 1)) | (pi & ((1 << q) - 1));
+        const int hi = lo | (1 << q);
+        const V x = s[lo], y = s[hi];
+        V nx, ny;  // c x + i sn y
+        nx.x = c * x.x - sn * y.y;
+        nx.y = c * x.y + sn * y.x;
+        ny.x = c * y.x - sn * x.y;
+        ny.y = c * y.y + sn * x.x;
+        s[lo] = nx;
+        s[hi] = ny;
+      }
+      __syncthreads();
+    }
+  }
+  V* g = reinterpret_cast<V*>(P.amps);
+  for (int z = t; z < N; z += blockDim.x) g[z] = s[z];
+  if (P.W == nullptr) return;
+  double sp = 0.0, spe = 0.0, mine = __longlong_as_double(0x7ff0000000000000ll);
+  unsigned long long zb = ~0ull;
+  for (int z = t; z < N; z += blockDim.x) {
+    double e = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = i + 1; j < n; ++j) e += P.W[i * n + j] * spin(z, i) * spin(z, j);
+    const double pv = prob(s[z]);
+    sp += pv;
+    spe = fma(pv, e, spe);
+    const bool ok = P.min_bit == -1 || (P.min_bit >= 0 && !((z >> P.min_bit) & 1));
+    if (ok && (e < mine || (e == mine && (unsigned long long)z < zb))) {
+      mine = e;
+      zb = z;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sp += __shfl_xor_sync(0xffffffffu, sp, o);
+    spe += __shfl_xor_sync(0xffffffffu, spe, o);
+    const double om = __shfl_xor_sync(0xffffffffu, mine, o);
+    const unsigned long long oz = __shfl_xor_sync(0xffffffffu, zb, o);
+    if (om < mine || (om == mine && oz < zb)) {
+      mine = om;
+      zb = oz;
+    }
+  }
+  if ((t & 31) == 0) {
+    red[(t >> 5) * 4 + 0] = sp;
+    red[(t >> 5) * 4 + 1] = spe;
+    red[(t >> 5) * 4 + 2] = mine;
+    red[(t >> 5) * 4 + 3] = __longlong_as_double((long long)zb);
+  }
+  __syncthreads();
+  if (t == 0) {
+    double s0 = 0.0, s1 = 0.0, mn = red[2];
+    unsigned long long b = (unsigned long long)__double_as_longlong(red[3]);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      s0 += red[w * 4];
+      s1 += red[w * 4 + 1];
+      const double om = red[w * 4 + 2];
+      const unsigned long long oz = (unsigned long long)__double_as_longlong(red[w * 4 + 3]);
+      if (om < mn || (om == mn && oz < b)) {
+        mn = om;
+        b = oz;
+      }
+    }
+    P.red_p[0] = s0;
+    P.red_pE[0] = s1;
+    P.red_minE[0] = mn;
+    P.red_arg[0] = b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic combine of the per-tile partials + exclusive CDF prefix over
+// tiles.  One CTA; each thread owns a contiguous run of tiles; fixed order.
+// out[0] = sum p, out[1] = sum p*E_w, out[2] = min E_w, out[3] = argmin (bits)
+__global__ void __launch_bounds__(1024) finalize_kernel(long long T, const double* __restrict__ rp,
+                                                         const double* __restrict__ rpe,
+                                                         const double* __restrict__ rmin,
+                                                         const unsigned long long* __restrict__ rarg,
+                                                         double* __restrict__ prefix, double* __restrict__ out) {
+  __shared__ double s_p[1024], s_pe[1024], s_min[1024];
+  __shared__ unsigned long long s_arg[1024];
+  const int t = threadIdx.x, NTH = blockDim.x;
+  const long long per = (T + NTH - 1) / NTH;
+  const long long lo = min(T, per * t), hi = min(T, lo + per);
+  double a = 0.0, b = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  unsigned long long z = ~0ull;
+  for (long long i = lo; i < hi; ++i) {
+    a += rp[i];
+    b += rpe[i];
+    const double m = rmin[i];
+    if (m < mn || (m == mn && rarg[i] < z)) {
+      mn = m;
+      z = rarg[i];
+    }
+  }
+  s_p[t] = a;
+  s_pe[t] = b;
+  s_min[t] = mn;
+  s_arg[t] = z;
+  __syncthreads();
+  if (t == 0) {
+    double acc = 0.0, accb = 0.0, m = s_min[0];
+    unsigned long long zz = s_arg[0];
+    for (int i = 0; i < NTH; ++i) {
+      const double x = s_p[i];
+      s_p[i] = acc;  // exclusive offset of thread i
+      acc += x;
+      accb += s_pe[i];
+      if (s_min[i] < m || (s_min[i] == m && s_arg[i] < zz)) {
+        m = s_min[i];
+        zz = s_arg[i];
+      }
+    }
+    out[0] = acc;
+    out[1] = accb;
+    out[2] = m;
+    out[3] = __longlong_as_double((long long)zz);
+    prefix[T] = acc;
+  }
+  __syncthreads();
+  double run = s_p[t];
+  for (long long i = lo; i < hi; ++i) {
+    prefix[i] = run;
+    run += rp[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Two-level inverse-CDF sampler (reference engine.py:254-263: first index
+// whose normalised cumulative probability exceeds u).  One warp per shot:
+// binary search over tile prefixes, then an in-tile scan in index order.
+template <typename T>
+__global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tiles, const double* __restrict__ prefix,
+                              const double* __restrict__ u, long long shots, unsigned long long* __restrict__ out) {
+  typedef typename CxT<T>::V V;
+  const V* amps = reinterpret_cast<const V*>(amps_);
+  const int lane = threadIdx.x & 31;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= shots) return;
+  const double total = prefix[T_tiles];
+  const double x = u[warp];
+  // first tile b with prefix[b+1] / total > x
+  long long lo = 0, hi = T_tiles - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (prefix[mid + 1] / total > x) hi = mid;
+    else lo = mid + 1;
+  }
+  const long long b = lo;
+  const long long L = 1ll << tile_bits;
+  const long long chunk = L >= 32 ? L / 32 : 1;
+  const long long e0 = lane * chunk;
+  double mine = 0.0;
+  const V* base = amps + (b << tile_bits);
+  if (e0 < L)
+    for (long long e = e0; e < e0 + chunk; ++e) mine += prob(base[e]);
+  // inclusive scan over lanes
+  double inc = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const double off = prefix[b];
+  const bool hit = e0 < L && (off + inc) / total > x;
+  const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+  long long idx;
+  if (ballot == 0) {
+    idx = (b << tile_bits) + L - 1;
+    if (lane == 0) out[warp] = (unsigned long long)idx;
+    return;
+  }
+  const int L0 = __ffs(ballot) - 1;
+  if (lane == L0) {
+    double c = off + inc - mine;
+    idx = e0 + chunk - 1;
+    for (long long e = e0; e < e0 + chunk; ++e) {
+      c += prob(base[e]);
+      if (c / total > x) {
+        idx = e;
+        break;
+      }
+    }
+    out[warp] = (unsigned long long)((b << tile_bits) + idx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bit-exact cut values (reference problem.py:139-149): sequential float64
+// accumulation over edges in lexicographic order; w*bit is exact, and the
+// adds are forced to round-to-nearest one by one (no reassociation).
+__global__ void cut_values_kernel(int n, const double* __restrict__ w, const unsigned long long* __restrict__ z,
+                                  long long count, unsigned long long start, double* __restrict__ out) {
+  extern __shared__ double ws[];
+  const int E = n * (n - 1) / 2;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) ws[i] = w[i];
+  __syncthreads();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+       k += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long x = z ? z[k] : start + (unsigned long long)k;
+    double acc = 0.0;
+    int e = 0;
+    for (int i = 0; i < n; ++i) {
+      const unsigned long long xi = x >> i;
+      for (int j = i + 1; j < n; ++j, ++e) {
+        const unsigned long long bit = (xi ^ (x >> j)) & 1ull;
+        acc = __dadd_rn(acc, bit ? ws[e] : 0.0);
+      }
+    }
+    out[k] = acc;
+  }
+}
+
+}  // namespace lrq

@@ -1,0 +1,98 @@
+// Device-side building blocks for the LR-QAOA state-vector engine (sm_100a).
+//
+// Notation used throughout:
+//   n      local qubits; amplitude index z has qubit k at bit k
+//          (reference convention, lrqbench engine.py:3-4).
+//   tile   2^K amplitudes handled by one CTA at a time.  Tile bit i maps to
+//          global bit g(i) = i for i < m, q0 + (i - m) for i >= m, so every
+//          tile is a union of 2^(K-m) contiguous runs of 2^m amplitudes.
+//   layout "lo": each thread holds 2^RB amplitudes in registers whose tile
+//          indices differ in tile bits [lo, lo+RB); the thread index fills the
+//          other tile bits in ascending order.
+//   E_M(z) = sum_{i<j} M_ij s_i s_j + sum_i ext_i s_i + cst,  s_k = 1 - 2 bit_k(z).
+//          With M = J_k (per-layer RZZ half angles) exp(-i E_J) is the cost
+//          phase of one layer; with M = w (edge weights) C(z) = (W - E_w)/2.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrq {
+
+template <typename T> struct CxT;
+template <> struct CxT<float> { typedef float2 V; };
+template <> struct CxT<double> { typedef double2 V; };
+
+__host__ __device__ constexpr int ctz_c(int k) { return (k & 1) ? 0 : 1 + ctz_c(k >> 1); }
+
+__device__ __forceinline__ double spin(uint64_t z, int k) { return ((z >> k) & 1ull) ? -1.0 : 1.0; }
+
+// ---------------------------------------------------------------------------
+// complex helpers
+
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long u;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(u) : "f"(a), "f"(b));
+  return u;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long u) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(u));
+  return r;
+}
+// packed a*b + c on two fp32 lanes (Blackwell FFMA2)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(r);
+}
+
+// x + i t y  (one half of the scaled RX butterfly)
+__device__ __forceinline__ float2 bf_half(float2 x, float2 y, float2 tv /* (-t, t) */) {
+  return ffma2(tv, make_float2(y.y, y.x), x);
+}
+__device__ __forceinline__ double2 bf_half(double2 x, double2 y, double t) {
+  return make_double2(fma(-t, y.y, x.x), fma(t, y.x, x.y));
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmul_conj(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cmul_amp(float2 a, double2 f) {
+  float2 g = make_float2((float)f.x, (float)f.y);
+  float2 m = fmul2(make_float2(a.y, a.y), make_float2(-g.y, g.x));
+  return ffma2(make_float2(a.x, a.x), g, m);
+}
+__device__ __forceinline__ double2 cmul_amp(double2 a, double2 f) { return cmul(a, f); }
+
+__device__ __forceinline__ double2 expmi(double angle) {  // exp(-i angle)
+  double s, c;
+  sincos(angle, &s, &c);
+  return make_double2(c, -s);
+}
+
+// ---------------------------------------------------------------------------
+// streaming global access (each amplitude is read once and written once per
+// sweep; the state is far larger than L2, so mark it evict-first)
+
+__device__ __forceinline__ float2 ld_amp(const float2* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_amp(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_amp(float2* p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_amp(double2* p, double2 v) { __stcs(p, v); }
+
+// |a|^2 in float64 with the reference's rounding: re*re and im*im each rounded,
+// then added (engine.py:94-96) — no FMA contraction.
+__device__ __forceinline__ double prob(float2 a) {
+  double x = (double)a.x, y = (double)a.y;
+  return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+}
+__device__ __forceinline__ double prob(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+}  // namespace lrq

@@ -1,0 +1,760 @@
+// liblrq.so — host engine and C ABI (include/lrq.h) for the B200-native
+// LR-QAOA state-vector path.  Replaces lrqbench engine.py:198-273 and
+// problem.py:139-211 behind the reference's own entry points (the Python
+// mirror in paper_2604_26423_b200 calls these through ctypes).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lrq.h"
+#include "lrq_aux.cuh"
+#include "lrq_plan.h"
+#include "lrq_sweep.cuh"
+
+using namespace lrq;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? LRQ_ECAPACITY : LRQ_ERUNTIME,             \
+                  std::string("CUDA error in ") + #expr + ": " + cudaGetErrorString(e_));    \
+    }                                                                                         \
+  } while (0)
+
+// tile geometry per precision
+constexpr int kNTB = 8;        // 256 threads per CTA
+constexpr int kRB64 = 5;       // complex64: 32 amplitudes per thread, K = 13
+constexpr int kRB128 = 4;      // complex128: 16 amplitudes per thread, K = 12
+constexpr int kKmax64 = 10;    // high groups: m >= 3 -> runs of >= 64 B
+constexpr int kKmax128 = 8;    // high groups: m >= 4 -> runs of >= 256 B
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+struct Geometry {
+  int NTB, RB, K, kmax;
+};
+Geometry geometry(int pbytes) {
+  Geometry g;
+  g.NTB = kNTB;
+  g.RB = pbytes == 8 ? kRB64 : kRB128;
+  g.K = g.NTB + g.RB;
+  g.kmax = env_int(pbytes == 8 ? "LRQ_KMAX64" : "LRQ_KMAX128", pbytes == 8 ? kKmax64 : kKmax128);
+  if (g.kmax < 1) g.kmax = 1;
+  if (g.kmax > g.K - 1) g.kmax = g.K - 1;
+  return g;
+}
+
+template <typename T, int NTB, int RB>
+int configure_sweep() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(sweep_kernel<T, NTB, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  CUDA_TRY(err);
+  return LRQ_OK;
+}
+
+int sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+  return v;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+std::string gib(double bytes) {
+  char b[64];
+  snprintf(b, sizeof b, "%.1f", bytes / (double)(1ull << 30));
+  return b;
+}
+
+}  // namespace
+
+struct lrq_state {
+  int n = 0;
+  int pbytes = 0;
+  int device = 0;
+  Geometry geo{};
+  cudaStream_t stream = nullptr;
+  void* amps = nullptr;
+  size_t state_bytes = 0;
+  long long num_tiles = 1;
+  double* red = nullptr;     // 4 arrays of num_tiles (p, pE, minE, arg bits)
+  double* prefix = nullptr;  // num_tiles + 1
+  double* out = nullptr;     // 4 finalize scalars
+  double* dW = nullptr;      // n*n cost matrix
+  double* dzero = nullptr;   // n zeros (no global qubits on a single device)
+  double* dJ = nullptr;      // p*n*n phase matrices
+  double* dmix = nullptr;    // p*2 (cos h, -sin h)
+  int jcap = 0;
+  double* du = nullptr;
+  unsigned long long* didx = nullptr;
+  long long shot_cap = 0;
+  bool have_cost = false, reduced = false, ran = false;
+  double wtot = 0.0;
+  bool timing = false;
+  std::vector<cudaEvent_t> evs;
+  std::vector<char> kinds;
+  std::vector<double> last_ms;
+};
+
+namespace {
+
+void free_state(lrq_state* s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  cudaFree(s->amps);
+  cudaFree(s->red);
+  cudaFree(s->prefix);
+  cudaFree(s->out);
+  cudaFree(s->dW);
+  cudaFree(s->dzero);
+  cudaFree(s->dJ);
+  cudaFree(s->dmix);
+  cudaFree(s->du);
+  cudaFree(s->didx);
+  for (cudaEvent_t e : s->evs) cudaEventDestroy(e);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+// sequential v_n: n products by fl(1/sqrt 2) in the state precision
+// (reference H kernel applied to |0..0>, engine.py:128-134)
+template <typename T>
+double init_amplitude(int n) {
+  const T r = (T)(1.0 / sqrt(2.0));
+  T v = (T)1.0;
+  for (int i = 0; i < n; ++i) v = v * r;
+  return (double)v;
+}
+
+void sym_matrix(int n, const double* e, double* M) {
+  memset(M, 0, sizeof(double) * n * n);
+  int k = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j, ++k) M[i * n + j] = M[j * n + i] = e[k];
+}
+
+struct MixerForm {
+  double t;
+  int swap;
+  double qre, qim;  // per-qubit scalar factor
+};
+MixerForm mixer_form(double h) {
+  // RX(theta) = cos(h) I - i sin(h) X, h = theta/2 (engine.py:137-144)
+  const double c = cos(h), s = -sin(h);
+  MixerForm f;
+  if (fabs(s) <= fabs(c)) {
+    f.t = s / c;
+    f.swap = 0;
+    f.qre = c;
+    f.qim = 0.0;
+  } else {
+    f.t = -c / s;
+    f.swap = 1;
+    f.qre = 0.0;
+    f.qim = s;
+  }
+  return f;
+}
+
+void cpow_mul(double& re, double& im, double qre, double qim, int k) {
+  for (int i = 0; i < k; ++i) {
+    const double r = re * qre - im * qim, m = re * qim + im * qre;
+    re = r;
+    im = m;
+  }
+}
+
+template <typename T, int NTB, int RB>
+int launch_sweep(lrq_state* s, const SweepParams& sp, int grid) {
+  int rc = configure_sweep<T, NTB, RB>();
+  if (rc) return rc;
+  const size_t smem = sweep_smem_bytes(sizeof(typename CxT<T>::V), NTB, RB, sp.n, sp.flags);
+  sweep_kernel<T, NTB, RB><<<grid, 1 << NTB, smem, s->stream>>>(sp);
+  CUDA_TRY(cudaGetLastError());
+  return LRQ_OK;
+}
+
+int launch_any_sweep(lrq_state* s, const SweepParams& sp, int grid) {
+  if (s->pbytes == 8) return launch_sweep<float, kNTB, kRB64>(s, sp, grid);
+  return launch_sweep<double, kNTB, kRB128>(s, sp, grid);
+}
+
+void record(lrq_state* s, size_t idx, char kind) {
+  if (!s->timing) return;
+  while (s->evs.size() <= idx) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    s->evs.push_back(e);
+  }
+  cudaEventRecord(s->evs[idx], s->stream);
+  if (kind) s->kinds.push_back(kind);
+}
+
+}  // namespace
+
+extern "C" {
+
+int lrq_abi_version(void) { return LRQ_ABI_VERSION; }
+
+const char* lrq_last_error(void) { return g_err.c_str(); }
+
+int lrq_device_count(int* count) {
+  if (!count) return fail(LRQ_EVALIDATION, "null count");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(LRQ_ERUNTIME, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  *count = c;
+  return LRQ_OK;
+}
+
+int lrq_describe_plan(int n, int pbytes, int p, char* buf, size_t cap) {
+  if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
+  if (n < 1 || n > 40) return fail(LRQ_EVALIDATION, "num_qubits out of range [1, 40]");
+  if (p < 1) return fail(LRQ_EVALIDATION, "p must be >= 1");
+  const Geometry g = geometry(pbytes);
+  const std::string js = plan_json(make_plan(n, g.NTB, g.RB, p, g.kmax));
+  if (!buf || cap < js.size() + 1) return fail(LRQ_EVALIDATION, "buffer too small: need " + std::to_string(js.size() + 1));
+  memcpy(buf, js.c_str(), js.size() + 1);
+  return LRQ_OK;
+}
+
+int lrq_create(int n, int pbytes, int device, uint64_t budget, lrq_state** out) {
+  if (!out) return fail(LRQ_EVALIDATION, "null output handle");
+  *out = nullptr;
+  if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
+  if (n < 1) return fail(LRQ_EVALIDATION, "need at least one qubit, got " + std::to_string(n));
+  if (n > 40) return fail(LRQ_ECAPACITY, "num_qubits > 40 is not supported on one device");
+  const size_t need = (size_t)pbytes << n;
+  const char* prec = pbytes == 8 ? "fp32" : "fp64";
+  if (budget && need > budget)
+    return fail(LRQ_ECAPACITY, "statevector for " + std::to_string(n) + " qubits at " + prec + " needs " +
+                                   std::to_string(need) + " bytes (" + gib((double)need) + " GiB), budget is " +
+                                   std::to_string(budget) + " bytes");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LRQ_ERUNTIME, "no CUDA device available (the LR-QAOA engine has no CPU path)");
+  if (device < 0 || device >= ndev) return fail(LRQ_EVALIDATION, "device index out of range");
+  DeviceGuard guard(device);
+  size_t freeb = 0, totalb = 0;
+  CUDA_TRY(cudaMemGetInfo(&freeb, &totalb));
+  if (need + (256ull << 20) > freeb)
+    return fail(LRQ_ECAPACITY, "statevector for " + std::to_string(n) + " qubits at " + prec + " needs " +
+                                   std::to_string(need) + " bytes (" + gib((double)need) +
+                                   " GiB), device has " + std::to_string(freeb) + " bytes free");
+  lrq_state* s = new lrq_state();
+  s->n = n;
+  s->pbytes = pbytes;
+  s->device = device;
+  s->geo = geometry(pbytes);
+  s->state_bytes = need;
+  s->num_tiles = n >= s->geo.K ? (1ll << (n - s->geo.K)) : 1;
+  cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&s->amps, need);
+  if (e == cudaSuccess) e = cudaMalloc(&s->red, sizeof(double) * 4 * s->num_tiles);
+  if (e == cudaSuccess) e = cudaMalloc(&s->prefix, sizeof(double) * (s->num_tiles + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&s->out, sizeof(double) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dW, sizeof(double) * n * n);
+  if (e == cudaSuccess) e = cudaMemset(s->dW, 0, sizeof(double) * n * n);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dzero, sizeof(double) * (n + 1));
+  if (e == cudaSuccess) e = cudaMemset(s->dzero, 0, sizeof(double) * (n + 1));
+  if (e != cudaSuccess) {
+    free_state(s);
+    return fail(e == cudaErrorMemoryAllocation ? LRQ_ECAPACITY : LRQ_ERUNTIME,
+                std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  *out = s;
+  return LRQ_OK;
+}
+
+int lrq_destroy(lrq_state* s) {
+  free_state(s);
+  return LRQ_OK;
+}
+
+int lrq_set_cost(lrq_state* s, const double* w) {
+  if (!s || !w) return fail(LRQ_EVALIDATION, "null argument");
+  const int n = s->n, E = n * (n - 1) / 2;
+  std::vector<double> M((size_t)n * n);
+  double tot = 0.0;
+  for (int e = 0; e < E; ++e) {
+    if (!isfinite(w[e])) return fail(LRQ_EVALIDATION, "edge weight is not finite");
+    tot += w[e];
+  }
+  sym_matrix(n, w, M.data());
+  DeviceGuard guard(s->device);
+  CUDA_TRY(cudaMemcpyAsync(s->dW, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->wtot = tot;
+  s->have_cost = true;
+  s->reduced = false;
+  return LRQ_OK;
+}
+
+int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (p < 1) return fail(LRQ_EVALIDATION, "depth p must be >= 1");
+  if (!phase || !mixer) return fail(LRQ_EVALIDATION, "null phase/mixer arrays");
+  const int n = s->n, E = n * (n - 1) / 2;
+  for (long long i = 0; i < (long long)p * E; ++i)
+    if (!isfinite(phase[i])) return fail(LRQ_EVALIDATION, "phase angle is not finite");
+  for (int k = 0; k < p; ++k)
+    if (!isfinite(mixer[k])) return fail(LRQ_EVALIDATION, "mixer angle is not finite");
+  DeviceGuard guard(s->device);
+  if (p > s->jcap) {
+    cudaFree(s->dJ);
+    cudaFree(s->dmix);
+    s->dJ = nullptr;
+    s->dmix = nullptr;
+    CUDA_TRY(cudaMalloc(&s->dJ, sizeof(double) * (size_t)p * n * n));
+    CUDA_TRY(cudaMalloc(&s->dmix, sizeof(double) * 2 * p));
+    s->jcap = p;
+  }
+  std::vector<double> J((size_t)p * n * n), mix(2 * p);
+  for (int k = 0; k < p; ++k) {
+    sym_matrix(n, phase + (size_t)k * E, J.data() + (size_t)k * n * n);
+    mix[2 * k] = cos(mixer[k]);
+    mix[2 * k + 1] = -sin(mixer[k]);
+  }
+  CUDA_TRY(cudaMemcpyAsync(s->dJ, J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(s->dmix, mix.data(), sizeof(double) * mix.size(), cudaMemcpyHostToDevice, s->stream));
+
+  const double init = s->pbytes == 8 ? init_amplitude<float>(n) : init_amplitude<double>(n);
+  s->reduced = false;
+  s->ran = false;
+  s->kinds.clear();
+  size_t ev = 0;
+  record(s, ev++, 0);
+  double* rp = s->red;
+  double* rpe = rp + s->num_tiles;
+  double* rmin = rpe + s->num_tiles;
+  unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
+  const int min_bit = n - 1;
+
+  if (n < s->geo.K) {
+    SmallParams sp;
+    sp.amps = s->amps;
+    sp.n = n;
+    sp.p = p;
+    sp.J = s->dJ;
+    sp.mix = s->dmix;
+    sp.W = s->have_cost ? s->dW : nullptr;
+    sp.init_re = init;
+    sp.init_im = 0.0;
+    sp.load = 0;
+    sp.min_bit = min_bit;
+    sp.red_p = rp;
+    sp.red_pE = rpe;
+    sp.red_minE = rmin;
+    sp.red_arg = rarg;
+    const size_t smem = (size_t)s->pbytes * (1u << n) + 8 * 4 * 8;
+    if (s->pbytes == 8) small_kernel<float><<<1, 256, smem, s->stream>>>(sp);
+    else small_kernel<double><<<1, 256, smem, s->stream>>>(sp);
+    CUDA_TRY(cudaGetLastError());
+    record(s, ev++, 'S');
+  } else {
+    const Plan P = make_plan(n, s->geo.NTB, s->geo.RB, p, s->geo.kmax);
+    const int grid_cap = 2 * sm_count(s->device);
+    const int grid = (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap);
+    for (const PlanSweep& w : P.sweeps) {
+      const PlanGroup& g = P.groups[w.group];
+      SweepParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.amps = s->amps;
+      sp.n = n;
+      sp.m = g.m;
+      sp.q0 = g.q0;
+      sp.num_tiles = s->num_tiles;
+      sp.nrounds = (int)w.rounds.size();
+      if (sp.nrounds > kMaxRounds) return fail(LRQ_ERUNTIME, "internal: too many rounds in sweep");
+      for (int r = 0; r < sp.nrounds; ++r) {
+        const PlanRound& R = w.rounds[r];
+        sp.rounds[r].lo = (int8_t)R.lo;
+        sp.rounds[r].m1 = (uint8_t)R.m1;
+        sp.rounds[r].m2 = (uint8_t)R.m2;
+        sp.rounds[r].flags = (uint8_t)((R.phase ? RD_PHASE : 0) | (R.reduce && s->have_cost ? RD_REDUCE : 0));
+      }
+      sp.store_lo = w.store_lo;
+      sp.flags = SW_STORE;
+      if (w.init) sp.flags |= SW_INIT;
+      if (w.phase >= 0) sp.flags |= SW_PHASE;
+      if (w.reduce && s->have_cost) sp.flags |= SW_REDUCE;
+      double sre = 1.0, sim = 0.0;
+      if (w.beta1 >= 0) {
+        const MixerForm f = mixer_form(mixer[w.beta1]);
+        sp.t1 = f.t;
+        sp.swap1 = f.swap;
+        cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
+      }
+      if (w.beta2 >= 0) {
+        const MixerForm f = mixer_form(mixer[w.beta2]);
+        sp.t2 = f.t;
+        sp.swap2 = f.swap;
+        cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
+      }
+      sp.scale_re = sre;
+      sp.scale_im = sim;
+      sp.init_re = init;
+      sp.init_im = 0.0;
+      sp.J.M = w.phase >= 0 ? s->dJ + (size_t)w.phase * n * n : nullptr;
+      sp.J.ext = s->dzero;
+      sp.J.cst = 0.0;
+      sp.W.M = s->dW;
+      sp.W.ext = s->dzero;
+      sp.W.cst = 0.0;
+      sp.min_bit = min_bit;
+      sp.red_p = rp;
+      sp.red_pE = rpe;
+      sp.red_minE = rmin;
+      sp.red_arg = rarg;
+      int rc = launch_any_sweep(s, sp, grid);
+      if (rc) return rc;
+      record(s, ev++, w.phase >= 0 ? (w.beta1 >= 0 ? 'F' : 'P') : (w.reduce ? 'R' : 'M'));
+    }
+  }
+  if (s->have_cost) {
+    finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
+    CUDA_TRY(cudaGetLastError());
+    record(s, ev++, 'Z');
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->timing) {
+    s->last_ms.clear();
+    for (size_t i = 1; i < ev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, s->evs[i - 1], s->evs[i]);
+      s->last_ms.push_back(ms);
+    }
+  }
+  s->ran = true;
+  s->reduced = s->have_cost;
+  return LRQ_OK;
+}
+
+int lrq_recompute(lrq_state* s) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (!s->ran) return fail(LRQ_ERUNTIME, "state holds no circuit result yet");
+  DeviceGuard guard(s->device);
+  const int n = s->n;
+  double* rp = s->red;
+  double* rpe = rp + s->num_tiles;
+  double* rmin = rpe + s->num_tiles;
+  unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
+  if (n < s->geo.K) {
+    SmallParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.amps = s->amps;
+    sp.n = n;
+    sp.p = 0;
+    sp.J = s->dW;
+    sp.mix = s->dzero;
+    sp.W = s->dW;
+    sp.load = 1;
+    sp.min_bit = n - 1;
+    sp.red_p = rp;
+    sp.red_pE = rpe;
+    sp.red_minE = rmin;
+    sp.red_arg = rarg;
+    const size_t smem = (size_t)s->pbytes * (1u << n) + 8 * 4 * 8;
+    if (s->pbytes == 8) small_kernel<float><<<1, 256, smem, s->stream>>>(sp);
+    else small_kernel<double><<<1, 256, smem, s->stream>>>(sp);
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    const int K = s->geo.K, RB = s->geo.RB;
+    SweepParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.amps = s->amps;
+    sp.n = n;
+    sp.m = K;
+    sp.q0 = K;
+    sp.num_tiles = s->num_tiles;
+    sp.nrounds = 1;
+    sp.rounds[0].lo = (int8_t)(K - RB);
+    sp.rounds[0].flags = RD_REDUCE;
+    sp.store_lo = K - RB;
+    sp.flags = SW_REDUCE;
+    sp.scale_re = 1.0;
+    sp.W.M = s->dW;
+    sp.W.ext = s->dzero;
+    sp.J.ext = s->dzero;
+    sp.min_bit = n - 1;
+    sp.red_p = rp;
+    sp.red_pE = rpe;
+    sp.red_minE = rmin;
+    sp.red_arg = rarg;
+    const int grid_cap = 2 * sm_count(s->device);
+    int rc = launch_any_sweep(s, sp, (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap));
+    if (rc) return rc;
+  }
+  finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->reduced = true;
+  return LRQ_OK;
+}
+
+int lrq_reduce(lrq_state* s, lrq_reduction* out) {
+  if (!s || !out) return fail(LRQ_EVALIDATION, "null argument");
+  if (!s->reduced) return fail(LRQ_ERUNTIME, "no reductions: set a cost and run the circuit first");
+  DeviceGuard guard(s->device);
+  double h[4];
+  CUDA_TRY(cudaMemcpyAsync(h, s->out, sizeof h, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  out->sum_p = h[0];
+  out->sum_p_cut = 0.5 * (s->wtot * h[0] - h[1]);
+  out->min_energy = h[2];
+  uint64_t z;
+  memcpy(&z, &h[3], 8);
+  out->argmax_cut = z;
+  return LRQ_OK;
+}
+
+int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
+  if (!s || !u || !idx) return fail(LRQ_EVALIDATION, "null argument");
+  if (shots < 1) return fail(LRQ_EVALIDATION, "shot count must be positive, got " + std::to_string(shots));
+  if (!s->reduced) return fail(LRQ_ERUNTIME, "no CDF: set a cost and run the circuit first");
+  DeviceGuard guard(s->device);
+  double total = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&total, s->out, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (!(total > 0.0)) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
+  if (shots > s->shot_cap) {
+    cudaFree(s->du);
+    cudaFree(s->didx);
+    s->du = nullptr;
+    s->didx = nullptr;
+    CUDA_TRY(cudaMalloc(&s->du, sizeof(double) * shots));
+    CUDA_TRY(cudaMalloc(&s->didx, sizeof(unsigned long long) * shots));
+    s->shot_cap = shots;
+  }
+  CUDA_TRY(cudaMemcpyAsync(s->du, u, sizeof(double) * shots, cudaMemcpyHostToDevice, s->stream));
+  const int tile_bits = s->n < s->geo.K ? s->n : s->geo.K;
+  const long long threads = shots * 32;
+  const int block = 256;
+  const long long grid = (threads + block - 1) / block;
+  if (s->pbytes == 8)
+    sample_kernel<float><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
+                                                                   shots, s->didx);
+  else
+    sample_kernel<double><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
+                                                                    shots, s->didx);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(idx, s->didx, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return LRQ_OK;
+}
+
+int lrq_copy_amps(lrq_state* s, uint64_t start, uint64_t count, void* host) {
+  if (!s || (!host && count)) return fail(LRQ_EVALIDATION, "null argument");
+  if (start + count > (1ull << s->n)) return fail(LRQ_EVALIDATION, "amplitude range out of bounds");
+  DeviceGuard guard(s->device);
+  CUDA_TRY(cudaMemcpyAsync(host, (const char*)s->amps + start * s->pbytes, count * s->pbytes, cudaMemcpyDeviceToHost,
+                           s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return LRQ_OK;
+}
+
+int lrq_cut_values(int n, const double* w, const uint64_t* z, uint64_t start, int64_t count, double* out,
+                   int device) {
+  if (n < 2 || n > 63) return fail(LRQ_EVALIDATION, "num_qubits out of range [2, 63]");
+  if (!w || !out || count < 0) return fail(LRQ_EVALIDATION, "null argument");
+  if (count == 0) return LRQ_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LRQ_ERUNTIME, "no CUDA device available (cut values have no CPU path)");
+  DeviceGuard guard(device);
+  const int E = n * (n - 1) / 2;
+  double *dw = nullptr, *dout = nullptr;
+  unsigned long long* dz = nullptr;
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaError_t e = cudaMalloc(&dw, sizeof(double) * E);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(double) * count);
+  if (e == cudaSuccess && z) e = cudaMalloc(&dz, sizeof(unsigned long long) * count);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dw, w, sizeof(double) * E, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && z) e = cudaMemcpyAsync(dz, z, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    const long long blocks = (count + 255) / 256;
+    cut_values_kernel<<<(unsigned)(blocks < 65535 ? blocks : 65535), 256, sizeof(double) * E, st>>>(
+        n, dw, dz, count, (unsigned long long)start, dout);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(dw);
+  cudaFree(dout);
+  cudaFree(dz);
+  cudaStreamDestroy(st);
+  CUDA_TRY(e);
+  return LRQ_OK;
+}
+
+int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* value) {
+  if (n < 2 || n > 48) return fail(LRQ_EVALIDATION, "num_qubits out of range [2, 48]");
+  if (!w || !argmax || !value) return fail(LRQ_EVALIDATION, "null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LRQ_ERUNTIME, "no CUDA device available (max cut has no CPU path)");
+  DeviceGuard guard(device);
+  const int NTB = kNTB, RB = kRB64, K = NTB + RB;
+  uint64_t best = 0;
+  if (n < K) {
+    // tiny: reuse the whole-state kernel with p = 0 (uniform state) for min E
+    lrq_state* s = nullptr;
+    int rc = lrq_create(n, 16, device, 0, &s);
+    if (rc) return rc;
+    rc = lrq_set_cost(s, w);
+    if (!rc) {
+      SmallParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.amps = s->amps;
+      sp.n = n;
+      sp.p = 0;
+      sp.J = s->dW;
+      sp.mix = s->dzero;
+      sp.W = s->dW;
+      sp.init_re = 1.0;
+      sp.min_bit = n - 1;
+      double* rp = s->red;
+      sp.red_p = rp;
+      sp.red_pE = rp + 1;
+      sp.red_minE = rp + 2;
+      sp.red_arg = reinterpret_cast<unsigned long long*>(rp + 3);
+      small_kernel<double><<<1, 256, (size_t)16 * (1u << n) + 256, s->stream>>>(sp);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaMemcpyAsync(&best, rp + 3, 8, cudaMemcpyDeviceToHost, s->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+      if (e != cudaSuccess) rc = fail(LRQ_ERUNTIME, std::string("max cut: ") + cudaGetErrorString(e));
+    }
+    lrq_destroy(s);
+    if (rc) return rc;
+  } else {
+    // exhaustive E_w scan over z with top bit 0 (complement symmetry), NOAMPS sweep
+    const long long tiles = 1ll << (n - K - 1 >= 0 ? n - K - 1 : 0);
+    const long long T = (n - 1 >= K) ? tiles : 1;
+    double *dW = nullptr, *red = nullptr, *prefix = nullptr, *out = nullptr, *zero = nullptr;
+    cudaStream_t st;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<double> M((size_t)n * n);
+    sym_matrix(n, w, M.data());
+    cudaError_t e = cudaMalloc(&dW, sizeof(double) * n * n);
+    if (e == cudaSuccess) e = cudaMalloc(&red, sizeof(double) * 4 * T);
+    if (e == cudaSuccess) e = cudaMalloc(&prefix, sizeof(double) * (T + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(double) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&zero, sizeof(double) * (n + 1));
+    if (e == cudaSuccess) e = cudaMemsetAsync(zero, 0, sizeof(double) * (n + 1), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(red, 0, sizeof(double) * 2 * T, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dW, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      int rc = configure_sweep<float, NTB, RB>();
+      if (rc) e = cudaErrorUnknown;
+    }
+    if (e == cudaSuccess) {
+      SweepParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.n = n;
+      sp.m = K;
+      sp.q0 = K;
+      sp.num_tiles = T;
+      sp.nrounds = 1;
+      sp.rounds[0].lo = (int8_t)(K - RB);
+      sp.rounds[0].flags = RD_REDUCE;
+      sp.store_lo = K - RB;
+      sp.flags = SW_NOAMPS | SW_REDUCE;
+      sp.scale_re = 1.0;
+      sp.W.M = dW;
+      sp.W.ext = zero;
+      sp.J.ext = zero;
+      sp.min_bit = n - 1;
+      sp.red_p = red;
+      sp.red_pE = red + T;
+      sp.red_minE = red + 2 * T;
+      sp.red_arg = reinterpret_cast<unsigned long long*>(red + 3 * T);
+      const int grid_cap = 2 * sm_count(device);
+      const int grid = (int)(T < grid_cap ? T : grid_cap);
+      const size_t smem = sweep_smem_bytes(8, NTB, RB, n, sp.flags);
+      sweep_kernel<float, NTB, RB><<<grid, 1 << NTB, smem, st>>>(sp);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      finalize_kernel<<<1, 1024, 0, st>>>(T, red, red + T, red + 2 * T,
+                                          reinterpret_cast<unsigned long long*>(red + 3 * T), prefix, out);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&best, out + 3, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dW);
+    cudaFree(red);
+    cudaFree(prefix);
+    cudaFree(out);
+    cudaFree(zero);
+    cudaStreamDestroy(st);
+    CUDA_TRY(e);
+  }
+  *argmax = best;
+  return lrq_cut_values(n, w, &best, 0, 1, value, device);
+}
+
+int lrq_set_timing(lrq_state* s, int enable) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  s->timing = enable != 0;
+  return LRQ_OK;
+}
+
+int lrq_get_timings(lrq_state* s, double* ms, char* kinds, int cap, int* count) {
+  if (!s || !count) return fail(LRQ_EVALIDATION, "null argument");
+  const int c = (int)s->last_ms.size();
+  *count = c;
+  for (int i = 0; i < c && i < cap; ++i) {
+    if (ms) ms[i] = s->last_ms[i];
+    if (kinds) kinds[i] = i < (int)s->kinds.size() ? s->kinds[i] : '?';
+  }
+  return LRQ_OK;
+}
+
+int lrq_stream(lrq_state* s, void** out) {
+  if (!s || !out) return fail(LRQ_EVALIDATION, "null argument");
+  *out = (void*)s->stream;
+  return LRQ_OK;
+}
+
+int lrq_synchronize(lrq_state* s) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  DeviceGuard guard(s->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return LRQ_OK;
+}
+
+}  // extern "C"
