@@ -209,6 +209,24 @@ int launch_any_sweep(lrq_state* s, const SweepParams& sp, int grid) {
   return launch_sweep<double, kNTB, kRB128>(s, sp, grid);
 }
 
+template <typename T>
+int launch_small(const SmallParams& sp, size_t smem, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(small_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  });
+  CUDA_TRY(err);
+  small_kernel<T><<<1, 256, smem, st>>>(sp);
+  CUDA_TRY(cudaGetLastError());
+  return LRQ_OK;
+}
+
+int launch_small_any(int pbytes, const SmallParams& sp, cudaStream_t st) {
+  const size_t smem = (size_t)pbytes * (1u << sp.n) + 8 * 4 * 8;
+  return pbytes == 8 ? launch_small<float>(sp, smem, st) : launch_small<double>(sp, smem, st);
+}
+
 void record(lrq_state* s, size_t idx, char kind) {
   if (!s->timing) return;
   while (s->evs.size() <= idx) {
@@ -379,10 +397,8 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
-    const size_t smem = (size_t)s->pbytes * (1u << n) + 8 * 4 * 8;
-    if (s->pbytes == 8) small_kernel<float><<<1, 256, smem, s->stream>>>(sp);
-    else small_kernel<double><<<1, 256, smem, s->stream>>>(sp);
-    CUDA_TRY(cudaGetLastError());
+    int rc = launch_small_any(s->pbytes, sp, s->stream);
+    if (rc) return rc;
     record(s, ev++, 'S');
   } else {
     const Plan P = make_plan(n, s->geo.NTB, s->geo.RB, p, s->geo.kmax);
@@ -487,10 +503,8 @@ int lrq_recompute(lrq_state* s) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
-    const size_t smem = (size_t)s->pbytes * (1u << n) + 8 * 4 * 8;
-    if (s->pbytes == 8) small_kernel<float><<<1, 256, smem, s->stream>>>(sp);
-    else small_kernel<double><<<1, 256, smem, s->stream>>>(sp);
-    CUDA_TRY(cudaGetLastError());
+    int rc = launch_small_any(s->pbytes, sp, s->stream);
+    if (rc) return rc;
   } else {
     const int K = s->geo.K, RB = s->geo.RB;
     SweepParams sp;
@@ -652,8 +666,8 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
       sp.red_pE = rp + 1;
       sp.red_minE = rp + 2;
       sp.red_arg = reinterpret_cast<unsigned long long*>(rp + 3);
-      small_kernel<double><<<1, 256, (size_t)16 * (1u << n) + 256, s->stream>>>(sp);
-      cudaError_t e = cudaGetLastError();
+      rc = launch_small_any(16, sp, s->stream);
+      cudaError_t e = rc ? cudaErrorUnknown : cudaSuccess;
       if (e == cudaSuccess) e = cudaMemcpyAsync(&best, rp + 3, 8, cudaMemcpyDeviceToHost, s->stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
       if (e != cudaSuccess) rc = fail(LRQ_ERUNTIME, std::string("max cut: ") + cudaGetErrorString(e));
