@@ -1,0 +1,380 @@
+"""Benchmark of the LR-QAOA state-vector hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--n 32] [--p 10] [--precision fp32] [--shots 1000]
+
+Workload (BASELINE.json configs[2], the largest single-GPU config inside the
+metric's n=30-36 range): fully connected weighted MaxCut LR-QAOA, n=32,
+p=10, complex64 (32 GiB state), instance generate_instance(32, 1), ramp
+0.2/0.2.  One step = the whole hot path on one batch: H layer + p layers
+(fused sweeps) + fused final pass (sum p, sum pC, max cut, CDF block sums)
++ 1k inverse-CDF samples.
+
+value   layer amplitude-updates/s = 2^n * p * steps / device time, summed over
+        ranks (device time = max over ranks of CUDA events on the engine stream).
+e2e     same metric through the public drop-in API (run_circuit ->
+        exact_expected_r -> sample) with host inputs/outputs inside the timed
+        region (H2D of the layer angles/weights/uniforms, D2H of r and shots).
+roofline  dominant kernel = sweep_kernel; algorithmic bytes per launch =
+        2 * 2^n * B (B = 8 for complex64; the first, write-only sweep 2^n*B),
+        divided by its CUDA-event duration on the engine stream.
+
+Multi-GPU (--gpus N under torchrun): N independent replicas of the workload,
+one per rank (weak scaling); see DESIGN.md §5 for the global-qubit path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+METRIC = "LR-QAOA layer amplitude-updates/s"
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=32)
+    ap.add_argument("--p", type=int, default=10)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--shots", type=int, default=1000)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the CPU reference sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def init_dist(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    return dist
+
+
+def max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profiled_traffic():
+    """dram read+write bytes per sweep launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the oracle port of the reference per-gate engine
+
+
+def cpu_reference(n, p, precision, budget_s, seed):
+    """Time the reference's per-gate numpy kernels (oracle port, all host cores)
+    on a bounded sample of the workload and extrapolate to one layer:
+    t_layer = E_n * t_RZZ + n * t_RX (lrqbench engine.py:137-155)."""
+    import psutil
+
+    from oracle import lrq_oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    B = 8 if precision == "fp32" else 16
+    avail = psutil.virtual_memory().available
+    n_run = n
+    n_run = min(n_run, 30)  # bounded sample: per-gate cost is linear in 2^n
+    while n_run > 16 and (3 * (B << n_run) > 0.6 * avail):
+        n_run -= 1
+    scale = float(1 << (n - n_run))
+    eng = O.DenseOracle(n_run, precision, threads=cores)
+    eng.amps[:] = eng.dtype.type(1.0 / np.sqrt(1 << n_run))
+    w = O.instance_weights(n_run, seed)
+    betas, gammas = O.ramp(p)
+    pairs = O.edge_pairs(n_run)
+    t_rzz, t_rx = [], []
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < budget_s or len(t_rx) < 2:
+        a, b = pairs[(7 * k) % len(pairs)]
+        s = time.perf_counter()
+        eng.rzz(a, b, 2.0 * gammas[0] * w[(7 * k) % len(pairs)])
+        t_rzz.append(time.perf_counter() - s)
+        if k % 3 == 0:
+            s = time.perf_counter()
+            eng.rx(k % n_run, -2.0 * betas[0])
+            t_rx.append(time.perf_counter() - s)
+        k += 1
+    eng.close()
+    E = n * (n - 1) // 2
+    t_layer = (E * float(np.median(t_rzz)) + n * float(np.median(t_rx))) * scale
+    value = (1 << n) / t_layer
+    sample = (f"{len(t_rzz)} RZZ + {len(t_rx)} RX gates of the reference per-gate engine at n={n_run} "
+              f"({precision}), median per-gate time x (E_n RZZ + n RX) per layer"
+              + (f", scaled x{int(scale)} to n={n} (host RAM)" if n_run != n else ""))
+    return {"value": value, "unit": "amp-updates/s", "cores": cores, "kind": "port", "sample": sample,
+            "t_layer_s": t_layer}
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args, rank, world, local_rank, dist):
+    os.environ.setdefault("LRQ_DEVICE", str(local_rank))
+    import paper_2604_26423_b200 as L
+    from paper_2604_26423_b200 import _native
+    from paper_2604_26423_b200.build import build
+
+    if rank == 0:
+        build()
+    barrier(dist)
+    import torch
+
+    dev_index = int(os.environ["LRQ_DEVICE"])
+    torch.cuda.set_device(dev_index)
+    n, p = args.n, args.p
+    B = 8 if args.precision == "fp32" else 16
+    inst = L.generate_instance(n, args.seed)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=p))
+    lay = L.lower_circuit(circ)
+    w = inst.weights()
+    u = L.derive_rng(1, "shots", 0).random(args.shots)
+
+    # --- device-resident measurement (value) --------------------------------
+    dev = _native.DeviceState(n, B)
+    dev.set_cost(w)
+    stream = torch.cuda.ExternalStream(dev.stream())
+    for _ in range(args.warmup):
+        dev.run(lay.phase, lay.mixer)
+        dev.sample(u)
+    dev.set_timing(True)
+    sweep_ms, kinds_all = [], ""
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev_index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            dev.run(lay.phase, lay.mixer)
+            ms, kinds = dev.timings()
+            sweep_ms += ms
+            kinds_all += kinds
+            dev.sample(u)
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    barrier(dist)
+    dev_ms = e0.elapsed_time(e1)
+    dev_ms_max = max_over_ranks(dist, dev_ms)
+    red = dev.reduce()
+    dev.close(park=False)
+    _native.drain_pool()
+
+    # --- end to end through the public API (e2e) ------------------------------
+    solved = L.WmcInstance(inst.num_vertices, inst.edges, inst.seed,
+                           L.OptimalCut(L.index_to_bitstring(int(red.argmax_cut), n),
+                                        float(L.cut_values(inst, [int(red.argmax_cut)])[0])))
+    for _ in range(1):
+        sv = L.run_circuit(circ, args.precision)
+        L.exact_expected_r(sv, solved)
+        L.sample(sv, args.shots, 1)
+        sv.release()
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sv = L.run_circuit(circ, args.precision)
+        r_exact = L.exact_expected_r(sv, solved)
+        shots = L.sample(sv, args.shots, 1)
+        sv.release()
+    e2e_s = time.perf_counter() - t0
+    e2e_s_max = max_over_ranks(dist, e2e_s)
+    r_sampled = L.approximation_ratio(solved, shots)
+    _native.drain_pool()
+
+    if rank != 0:
+        return None
+    # sweep kernels: kinds P (init, write-only), M, F, R; Z = finalize
+    sw = [(m, k) for m, k in zip(sweep_ms, kinds_all) if k in "PMFR"]
+    alg = sum((1 if k == "P" else 2) * (B << n) for _, k in sw)
+    sweep_time_s = sum(m for m, _ in sw) * 1e-3
+    per_launch_achieved = alg / sweep_time_s / 1e9
+    peak, peak_kind = measured_peak()
+    traffic = profiled_traffic()
+    launches_per_step = len(sweep_ms) // args.steps + 1  # + sample kernel
+    amp_updates = float(1 << n) * p * args.steps * world
+    E = n * (n - 1) // 2
+    h2d = lay.phase.nbytes + lay.mixer.nbytes + w.nbytes + args.shots * 8
+    d2h = args.shots * 8 + 32
+    cpu = cpu_reference(n, p, args.precision, args.cpu_seconds, args.seed) if world == 1 else None
+    out = {
+        "metric": METRIC,
+        "value": amp_updates / (dev_ms_max * 1e-3),
+        "unit": "amp-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dev_ms_max / args.steps,
+        "ms_per_layer": dev_ms_max / args.steps / p,
+        "gate_equiv_amp_updates_per_s": amp_updates * (E + n) / (dev_ms_max * 1e-3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 amplitudes, fp64 phases and reductions)" if B == 8 else "c128 (fp64)",
+        "data": "synthetic: generate_instance(n, seed) Philox weights, LrQaoaParams(p) default ramp",
+        "config": {"workload": f"LR-QAOA p={p}, n={n} fully connected weighted MaxCut, "
+                               f"{'complex64' if B == 8 else 'complex128'} on 1xB200 (BASELINE configs[2])",
+                   "n": n, "p": p, "precision": args.precision, "shots": args.shots,
+                   "state_bytes": B << n, "parallelism": f"replicas x{world}",
+                   "l2": "state (32 GiB) >> L2 (126 MB); no flush needed"},
+        "e2e": {"value": amp_updates / e2e_s_max, "unit": "amp-updates/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "run_circuit -> exact_expected_r -> sample (drop-in API, ctypes C-ABI)"},
+        "roofline": {"bound": "hbm", "achieved": per_launch_achieved, "peak": peak, "unit": "GB/s",
+                     "frac": per_launch_achieved / peak, "peak_source": peak_kind,
+                     "traffic": traffic.get(f"n{n}_{args.precision}") if traffic else None,
+                     "kernel": "sweep_kernel", "bytes_per_launch": 2 * (B << n),
+                     "launch_ms_avg": sweep_time_s * 1e3 / max(1, len(sw))},
+        "sweeps_per_step": len(sw) // args.steps,
+        "sweep_ms": {k: round(statistics.mean(m for m, kk in sw if kk == k), 3) for k in sorted(set(kinds_all)) if k in "PMFR"},
+        "gpu_launches": launches_per_step * args.steps,
+        "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "clocks": clk.summary(),
+        "results": {"exact_r": r_exact, "sampled_r": r_sampled, "sum_p": red.sum_p,
+                    "max_cut": solved.optimal_cut.value},
+    }
+    return out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cpu = cpu_reference(args.n, args.p, args.precision, args.cpu_seconds, args.seed)
+    t_step = cpu["t_layer_s"] * args.p
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": cpu["value"],
+        "unit": "amp-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64" if args.precision == "fp32" else "c128",
+        "data": "synthetic",
+        "config": {"workload": f"LR-QAOA p={args.p}, n={args.n}, reference per-gate CPU engine (oracle port)",
+                   "n": args.n, "p": args.p, "precision": args.precision},
+        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cpu["value"], "unit": "amp-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        dist = init_dist(world)
+        out = run_ours(args, rank, world, local_rank, dist)
+        if dist is not None:
+            dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

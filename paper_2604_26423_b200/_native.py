@@ -109,6 +109,18 @@ def ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
+# One parked lrq_state per (n, precision, device): run_circuit in a loop then
+# reuses the HBM allocation instead of cudaFree/cudaMalloc of the whole state.
+_POOL: dict = {}
+
+
+def drain_pool() -> None:
+    """Free every parked device state."""
+    while _POOL:
+        _, h = _POOL.popitem()
+        lib().lrq_destroy(h)
+
+
 class DeviceState:
     """Owning handle of one lrq_state (a state vector in HBM)."""
 
@@ -117,6 +129,12 @@ class DeviceState:
         self.n = n
         self.precision_bytes = precision_bytes
         self.device = default_device() if device is None else int(device)
+        key = (n, precision_bytes, self.device)
+        h = _POOL.pop(key, None)
+        if h is not None:
+            self._h = h
+            self.set_cost(np.zeros(n * (n - 1) // 2))
+            return
         h = _state_p()
         check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
         self._h = h
@@ -127,9 +145,15 @@ class DeviceState:
             raise StateError("device state has been released")
         return self._h
 
-    def close(self) -> None:
+    def close(self, park: bool = True) -> None:
+        """Release the state; the allocation is parked for reuse unless the
+        pool already holds one for this shape (or park=False)."""
         if self._h is not None and _lib is not None:
-            _lib.lrq_destroy(self._h)
+            key = (self.n, self.precision_bytes, self.device)
+            if park and key not in _POOL:
+                _POOL[key] = self._h
+            else:
+                _lib.lrq_destroy(self._h)
         self._h = None
 
     def __del__(self):  # pragma: no cover - interpreter shutdown order
