@@ -267,3 +267,17 @@ __global__ void cut_values_kernel(int n, const double* __restrict__ w, const uns
 }
 
 }  // namespace lrq
+
+namespace lrq {
+// element z <-> element 2^bits - 1 - z (the global bit flip X^(x)n on indices)
+template <typename E>
+__global__ void reverse_kernel(void* data, int bits) {
+  E* a = reinterpret_cast<E*>(data);
+  const long long N = 1ll << bits;
+  const long long z = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (bits <= 0 || z >= N / 2) return;
+  const E x = a[z];
+  a[z] = a[N - 1 - z];
+  a[N - 1 - z] = x;
+}
+}  // namespace lrq

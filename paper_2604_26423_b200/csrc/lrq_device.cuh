@@ -53,7 +53,11 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 
 // x + i t y  (one half of the scaled RX butterfly)
 __device__ __forceinline__ float2 bf_half(float2 x, float2 y, float2 tv /* (-t, t) */) {
+#ifdef LRQ_EXPLICIT_FFMA2
   return ffma2(tv, make_float2(y.y, y.x), x);
+#else
+  return make_float2(fmaf(tv.x, y.y, x.x), fmaf(tv.y, y.x, x.y));
+#endif
 }
 __device__ __forceinline__ double2 bf_half(double2 x, double2 y, double t) {
   return make_double2(fma(-t, y.y, x.x), fma(t, y.x, x.y));
@@ -78,14 +82,31 @@ __device__ __forceinline__ double2 expmi(double angle) {  // exp(-i angle)
   return make_double2(c, -s);
 }
 
+// float32 phasor exp(-i angle) of a float64 angle: reduced mod 2pi in float64
+// first (|angle| reaches ~1e2 rad), then an accurate float32 sincos
+__device__ __forceinline__ float2 phasor32(double angle) {
+  const double k = rint(angle * 0.15915494309189535);
+  const float r = (float)fma(-k, 6.283185307179586, angle);
+  float s, co;
+  sincosf(r, &s, &co);
+  return make_float2(co, -s);
+}
+__device__ __forceinline__ float2 cmul32(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmul32_conj(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 conj32(float2 a) { return make_float2(a.x, -a.y); }
+
 // ---------------------------------------------------------------------------
 // streaming global access (each amplitude is read once and written once per
 // sweep; the state is far larger than L2, so mark it evict-first)
 
-__device__ __forceinline__ float2 ld_amp(const float2* p) { return __ldcs(p); }
-__device__ __forceinline__ double2 ld_amp(const double2* p) { return __ldcs(p); }
-__device__ __forceinline__ void st_amp(float2* p, float2 v) { __stcs(p, v); }
-__device__ __forceinline__ void st_amp(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ float4 ld_unit(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_unit(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_unit(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_unit(double2* p, double2 v) { __stcs(p, v); }
 
 // |a|^2 in float64 with the reference's rounding: re*re and im*im each rounded,
 // then added (engine.py:94-96) — no FMA contraction.

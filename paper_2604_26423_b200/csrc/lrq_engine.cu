@@ -14,7 +14,7 @@
 #include "../../include/lrq.h"
 #include "lrq_aux.cuh"
 #include "lrq_plan.h"
-#include "lrq_sweep.cuh"
+#include "lrq_sweep_kernel.cuh"
 
 using namespace lrq;
 
@@ -36,41 +36,50 @@ int fail(int code, const std::string& msg) {
     }                                                                                         \
   } while (0)
 
-// tile geometry per precision
-constexpr int kNTB = 8;        // 256 threads per CTA
-constexpr int kRB64 = 5;       // complex64: 32 amplitudes per thread, K = 13
-constexpr int kRB128 = 4;      // complex128: 16 amplitudes per thread, K = 12
-constexpr int kKmax64 = 10;    // high groups: m >= 3 -> runs of >= 64 B
-constexpr int kKmax128 = 8;    // high groups: m >= 4 -> runs of >= 256 B
+// tile geometry: 4096 16-byte units per tile = 2^(12+pair)
+// amplitudes (pair = 1 for complex64: a unit holds two amplitudes)
+inline int pair_of(int pbytes) { return pbytes == 8 ? 1 : 0; }
+inline int tile_amp_bits(int pbytes) { return kUnitBits + pair_of(pbytes); }
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
-struct Geometry {
-  int NTB, RB, K, kmax;
-};
-Geometry geometry(int pbytes) {
-  Geometry g;
-  g.NTB = kNTB;
-  g.RB = pbytes == 8 ? kRB64 : kRB128;
-  g.K = g.NTB + g.RB;
-  g.kmax = env_int(pbytes == 8 ? "LRQ_KMAX64" : "LRQ_KMAX128", pbytes == 8 ? kKmax64 : kKmax128);
-  if (g.kmax < 1) g.kmax = 1;
-  if (g.kmax > g.K - 1) g.kmax = g.K - 1;
-  return g;
-}
-
-template <typename T, int NTB, int RB>
-int configure_sweep() {
+template <typename T, int GK, int SK>
+int launch_sweep_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(sweep_kernel<T, NTB, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    err = cudaFuncSetAttribute(sweep_kernel<T, GK, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   CUDA_TRY(err);
+  sweep_kernel<T, GK, SK><<<grid, kThreads, smem, st>>>(sp);
+  CUDA_TRY(cudaGetLastError());
   return LRQ_OK;
+}
+
+template <typename T>
+int launch_sweep_kind(cudaStream_t st, int gk, int sk, const SweepParams& sp, int grid, size_t smem) {
+  if (gk == GK_A) {
+    switch (sk) {
+      case SK_P: return launch_sweep_t<T, GK_A, SK_P>(st, sp, grid, smem);
+      case SK_M: return launch_sweep_t<T, GK_A, SK_M>(st, sp, grid, smem);
+      case SK_F: return launch_sweep_t<T, GK_A, SK_F>(st, sp, grid, smem);
+      case SK_R: return launch_sweep_t<T, GK_A, SK_R>(st, sp, grid, smem);
+      case SK_L: return launch_sweep_t<T, GK_A, SK_L>(st, sp, grid, smem);
+      case SK_Q: return launch_sweep_t<T, GK_A, SK_Q>(st, sp, grid, smem);
+      case SK_N: return launch_sweep_t<T, GK_A, SK_N>(st, sp, grid, smem);
+    }
+  } else if (gk == GK_H) {
+    switch (sk) {
+      case SK_P: return launch_sweep_t<T, GK_H, SK_P>(st, sp, grid, smem);
+      case SK_M: return launch_sweep_t<T, GK_H, SK_M>(st, sp, grid, smem);
+      case SK_F: return launch_sweep_t<T, GK_H, SK_F>(st, sp, grid, smem);
+    }
+  } else if constexpr (sizeof(T) == 4) {
+    switch (sk) {
+      case SK_P: return launch_sweep_t<T, GK_H4, SK_P>(st, sp, grid, smem);
+      case SK_M: return launch_sweep_t<T, GK_H4, SK_M>(st, sp, grid, smem);
+      case SK_F: return launch_sweep_t<T, GK_H4, SK_F>(st, sp, grid, smem);
+    }
+  }
+  return fail(LRQ_ERUNTIME, "internal: no sweep kernel for this (group, kind)");
 }
 
 int sm_count(int device) {
@@ -102,7 +111,7 @@ struct lrq_state {
   int n = 0;
   int pbytes = 0;
   int device = 0;
-  Geometry geo{};
+  int K = 13;  // tile amp bits
   cudaStream_t stream = nullptr;
   void* amps = nullptr;
   size_t state_bytes = 0;
@@ -163,27 +172,41 @@ void sym_matrix(int n, const double* e, double* M) {
     for (int j = i + 1; j < n; ++j, ++k) M[i * n + j] = M[j * n + i] = e[k];
 }
 
+// RX(theta) = cos(h) I - i sin(h) X = c I + i s X, h = theta/2 (engine.py:137-144).
+// |s| <= |c|:  c (I + i t X) with t = s/c                      (flip = 0)
+// |s| >  |c|:  (i s) X (I + i t X) with t = -c/s               (flip = 1)
+// A layer applies the mixer to every qubit, so a flipped layer contributes
+// X^(x)n, which commutes with every cost phase (E(~z) = E(z)) and mixer: it is
+// deferred to one global index reversal at the end of the run.
 struct MixerForm {
   double t;
-  int swap;
+  int flip;
   double qre, qim;  // per-qubit scalar factor
 };
 MixerForm mixer_form(double h) {
-  // RX(theta) = cos(h) I - i sin(h) X, h = theta/2 (engine.py:137-144)
   const double c = cos(h), s = -sin(h);
   MixerForm f;
   if (fabs(s) <= fabs(c)) {
     f.t = s / c;
-    f.swap = 0;
+    f.flip = 0;
     f.qre = c;
     f.qim = 0.0;
   } else {
     f.t = -c / s;
-    f.swap = 1;
+    f.flip = 1;
     f.qre = 0.0;
     f.qim = s;
   }
   return f;
+}
+
+void fill_tangents(SweepParams& sp, int w, const unsigned* masks, int nrounds, double t) {
+  for (int r = 0; r < nrounds; ++r)
+    for (int a = 0; a < 5; ++a) {
+      const double v = ((masks[r] >> a) & 1u) ? t : 0.0;
+      sp.tf[w][r][a] = (float)v;
+      sp.td[w][r][a] = v;
+    }
 }
 
 void cpow_mul(double& re, double& im, double qre, double qim, int k) {
@@ -194,19 +217,13 @@ void cpow_mul(double& re, double& im, double qre, double qim, int k) {
   }
 }
 
-template <typename T, int NTB, int RB>
-int launch_sweep(lrq_state* s, const SweepParams& sp, int grid) {
-  int rc = configure_sweep<T, NTB, RB>();
-  if (rc) return rc;
-  const size_t smem = sweep_smem_bytes(sizeof(typename CxT<T>::V), NTB, RB, sp.n, sp.flags);
-  sweep_kernel<T, NTB, RB><<<grid, 1 << NTB, smem, s->stream>>>(sp);
-  CUDA_TRY(cudaGetLastError());
-  return LRQ_OK;
-}
-
-int launch_any_sweep(lrq_state* s, const SweepParams& sp, int grid) {
-  if (s->pbytes == 8) return launch_sweep<float, kNTB, kRB64>(s, sp, grid);
-  return launch_sweep<double, kNTB, kRB128>(s, sp, grid);
+int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp, int grid) {
+  const bool amps = sk != SK_N;
+  const bool usesJ = sk == SK_P || sk == SK_F || sk == SK_L;
+  const bool usesW = sk == SK_R || sk == SK_Q || sk == SK_N || (sk == SK_L && sp.reduce);
+  const size_t smem = sweep_smem_bytes(sp.n, amps, usesJ, usesW);
+  if (s->pbytes == 8) return launch_sweep_kind<float>(s->stream, gk, sk, sp, grid, smem);
+  return launch_sweep_kind<double>(s->stream, gk, sk, sp, grid, smem);
 }
 
 template <typename T>
@@ -262,8 +279,7 @@ int lrq_describe_plan(int n, int pbytes, int p, char* buf, size_t cap) {
   if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
   if (n < 1 || n > 40) return fail(LRQ_EVALIDATION, "num_qubits out of range [1, 40]");
   if (p < 1) return fail(LRQ_EVALIDATION, "p must be >= 1");
-  const Geometry g = geometry(pbytes);
-  const std::string js = plan_json(make_plan(n, g.NTB, g.RB, p, g.kmax));
+  const std::string js = plan_json(make_plan(n, pair_of(pbytes), p));
   if (!buf || cap < js.size() + 1) return fail(LRQ_EVALIDATION, "buffer too small: need " + std::to_string(js.size() + 1));
   memcpy(buf, js.c_str(), js.size() + 1);
   return LRQ_OK;
@@ -296,9 +312,9 @@ int lrq_create(int n, int pbytes, int device, uint64_t budget, lrq_state** out) 
   s->n = n;
   s->pbytes = pbytes;
   s->device = device;
-  s->geo = geometry(pbytes);
+  s->K = tile_amp_bits(pbytes);
   s->state_bytes = need;
-  s->num_tiles = n >= s->geo.K ? (1ll << (n - s->geo.K)) : 1;
+  s->num_tiles = n >= s->K ? (1ll << (n - s->K)) : 1;
   cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&s->amps, need);
   if (e == cudaSuccess) e = cudaMalloc(&s->red, sizeof(double) * 4 * s->num_tiles);
@@ -381,7 +397,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
   const int min_bit = n - 1;
 
-  if (n < s->geo.K) {
+  if (n < s->K) {
     SmallParams sp;
     sp.amps = s->amps;
     sp.n = n;
@@ -401,7 +417,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
     if (rc) return rc;
     record(s, ev++, 'S');
   } else {
-    const Plan P = make_plan(n, s->geo.NTB, s->geo.RB, p, s->geo.kmax);
+    const Plan P = make_plan(n, pair_of(s->pbytes), p);
     const int grid_cap = 2 * sm_count(s->device);
     const int grid = (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap);
     for (const PlanSweep& w : P.sweeps) {
@@ -410,41 +426,25 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       memset(&sp, 0, sizeof sp);
       sp.amps = s->amps;
       sp.n = n;
-      sp.m = g.m;
       sp.q0 = g.q0;
       sp.num_tiles = s->num_tiles;
-      sp.nrounds = (int)w.rounds.size();
-      if (sp.nrounds > kMaxRounds) return fail(LRQ_ERUNTIME, "internal: too many rounds in sweep");
-      for (int r = 0; r < sp.nrounds; ++r) {
-        const PlanRound& R = w.rounds[r];
-        sp.rounds[r].lo = (int8_t)R.lo;
-        sp.rounds[r].m1 = (uint8_t)R.m1;
-        sp.rounds[r].m2 = (uint8_t)R.m2;
-        sp.rounds[r].flags = (uint8_t)((R.phase ? RD_PHASE : 0) | (R.reduce && s->have_cost ? RD_REDUCE : 0));
-      }
-      sp.store_lo = w.store_lo;
-      sp.flags = SW_STORE;
-      if (w.init) sp.flags |= SW_INIT;
-      if (w.phase >= 0) sp.flags |= SW_PHASE;
-      if (w.reduce && s->have_cost) sp.flags |= SW_REDUCE;
+      sp.reduce = w.reduce ? 1 : 0;
       double sre = 1.0, sim = 0.0;
       if (w.beta1 >= 0) {
         const MixerForm f = mixer_form(mixer[w.beta1]);
-        sp.t1 = f.t;
-        sp.swap1 = f.swap;
+        fill_tangents(sp, 0, w.mask1, w.nrounds, f.t);
         cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
       }
       if (w.beta2 >= 0) {
         const MixerForm f = mixer_form(mixer[w.beta2]);
-        sp.t2 = f.t;
-        sp.swap2 = f.swap;
+        fill_tangents(sp, 1, w.mask2, w.nrounds, f.t);
         cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
       }
       sp.scale_re = sre;
       sp.scale_im = sim;
       sp.init_re = init;
       sp.init_im = 0.0;
-      sp.J.M = w.phase >= 0 ? s->dJ + (size_t)w.phase * n * n : nullptr;
+      sp.J.M = w.phase >= 0 ? s->dJ + (size_t)w.phase * n * n : s->dW;
       sp.J.ext = s->dzero;
       sp.J.cst = 0.0;
       sp.W.M = s->dW;
@@ -455,16 +455,29 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.red_pE = rpe;
       sp.red_minE = rmin;
       sp.red_arg = rarg;
-      int rc = launch_any_sweep(s, sp, grid);
+      int rc = launch_sweep(s, g.kind, w.kind, sp, grid);
       if (rc) return rc;
-      record(s, ev++, w.phase >= 0 ? (w.beta1 >= 0 ? 'F' : 'P') : (w.reduce ? 'R' : 'M'));
+      record(s, ev++, "PMFRLQN"[w.kind]);
+    }
+    int flips = 0;
+    for (int k = 0; k < p; ++k) flips += mixer_form(mixer[k]).flip;
+    if (flips & 1) {
+      // deferred X^(x)n of the flipped layers: reverse the index order once;
+      // tile b of the CDF becomes tile T-1-b (E and the max-cut are invariant)
+      const long long half = (1ll << n) / 2;
+      const unsigned blocks = (unsigned)((half + 255) / 256);
+      if (s->pbytes == 8) reverse_kernel<float2><<<blocks, 256, 0, s->stream>>>(s->amps, n);
+      else reverse_kernel<double2><<<blocks, 256, 0, s->stream>>>(s->amps, n);
+      CUDA_TRY(cudaGetLastError());
+      reverse_kernel<double><<<(unsigned)((s->num_tiles / 2 + 255) / 256 + 1), 256, 0, s->stream>>>(
+          rp, 63 - __builtin_clzll((unsigned long long)s->num_tiles));
+      CUDA_TRY(cudaGetLastError());
+      record(s, ev++, 'X');
     }
   }
-  if (s->have_cost) {
-    finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
-    CUDA_TRY(cudaGetLastError());
-    record(s, ev++, 'Z');
-  }
+  finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
+  CUDA_TRY(cudaGetLastError());
+  record(s, ev++, 'Z');
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   if (s->timing) {
     s->last_ms.clear();
@@ -475,7 +488,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
     }
   }
   s->ran = true;
-  s->reduced = s->have_cost;
+  s->reduced = true;
   return LRQ_OK;
 }
 
@@ -488,7 +501,7 @@ int lrq_recompute(lrq_state* s) {
   double* rpe = rp + s->num_tiles;
   double* rmin = rpe + s->num_tiles;
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
-  if (n < s->geo.K) {
+  if (n < s->K) {
     SmallParams sp;
     memset(&sp, 0, sizeof sp);
     sp.amps = s->amps;
@@ -506,30 +519,25 @@ int lrq_recompute(lrq_state* s) {
     int rc = launch_small_any(s->pbytes, sp, s->stream);
     if (rc) return rc;
   } else {
-    const int K = s->geo.K, RB = s->geo.RB;
     SweepParams sp;
     memset(&sp, 0, sizeof sp);
     sp.amps = s->amps;
     sp.n = n;
-    sp.m = K;
-    sp.q0 = K;
+    sp.q0 = s->K;
     sp.num_tiles = s->num_tiles;
-    sp.nrounds = 1;
-    sp.rounds[0].lo = (int8_t)(K - RB);
-    sp.rounds[0].flags = RD_REDUCE;
-    sp.store_lo = K - RB;
-    sp.flags = SW_REDUCE;
+    sp.reduce = 1;
     sp.scale_re = 1.0;
+    sp.J.M = s->dW;
+    sp.J.ext = s->dzero;
     sp.W.M = s->dW;
     sp.W.ext = s->dzero;
-    sp.J.ext = s->dzero;
     sp.min_bit = n - 1;
     sp.red_p = rp;
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
     const int grid_cap = 2 * sm_count(s->device);
-    int rc = launch_any_sweep(s, sp, (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap));
+    int rc = launch_sweep(s, GK_A, SK_Q, sp, (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap));
     if (rc) return rc;
   }
   finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
@@ -574,7 +582,7 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
     s->shot_cap = shots;
   }
   CUDA_TRY(cudaMemcpyAsync(s->du, u, sizeof(double) * shots, cudaMemcpyHostToDevice, s->stream));
-  const int tile_bits = s->n < s->geo.K ? s->n : s->geo.K;
+  const int tile_bits = s->n < s->K ? s->n : s->K;
   const long long threads = shots * 32;
   const int block = 256;
   const long long grid = (threads + block - 1) / block;
@@ -642,7 +650,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(LRQ_ERUNTIME, "no CUDA device available (max cut has no CPU path)");
   DeviceGuard guard(device);
-  const int NTB = kNTB, RB = kRB64, K = NTB + RB;
+  const int K = tile_amp_bits(8);
   uint64_t best = 0;
   if (n < K) {
     // tiny: reuse the whole-state kernel with p = 0 (uniform state) for min E
@@ -692,24 +700,16 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
     if (e == cudaSuccess) e = cudaMemsetAsync(red, 0, sizeof(double) * 2 * T, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dW, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
-      int rc = configure_sweep<float, NTB, RB>();
-      if (rc) e = cudaErrorUnknown;
-    }
-    if (e == cudaSuccess) {
       SweepParams sp;
       memset(&sp, 0, sizeof sp);
       sp.n = n;
-      sp.m = K;
       sp.q0 = K;
       sp.num_tiles = T;
-      sp.nrounds = 1;
-      sp.rounds[0].lo = (int8_t)(K - RB);
-      sp.rounds[0].flags = RD_REDUCE;
-      sp.store_lo = K - RB;
-      sp.flags = SW_NOAMPS | SW_REDUCE;
+      sp.reduce = 1;
       sp.scale_re = 1.0;
       sp.W.M = dW;
       sp.W.ext = zero;
+      sp.J.M = dW;
       sp.J.ext = zero;
       sp.min_bit = n - 1;
       sp.red_p = red;
@@ -718,9 +718,8 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
       sp.red_arg = reinterpret_cast<unsigned long long*>(red + 3 * T);
       const int grid_cap = 2 * sm_count(device);
       const int grid = (int)(T < grid_cap ? T : grid_cap);
-      const size_t smem = sweep_smem_bytes(8, NTB, RB, n, sp.flags);
-      sweep_kernel<float, NTB, RB><<<grid, 1 << NTB, smem, st>>>(sp);
-      e = cudaGetLastError();
+      const size_t smem = sweep_smem_bytes(n, false, false, true);
+      if (launch_sweep_t<float, GK_A, SK_N>(st, sp, grid, smem) != LRQ_OK) e = cudaErrorUnknown;
     }
     if (e == cudaSuccess) {
       finalize_kernel<<<1, 1024, 0, st>>>(T, red, red + T, red + 2 * T,

@@ -1,207 +1,186 @@
-// Host-side sweep planner (pure C++, no CUDA): turns (n, precision, p) into
-// the list of sweeps the engine launches.  See DESIGN.md §3.1.
+// Host-side sweep planner: turns (n, precision, p) into the list of sweeps the
+// engine launches.  See DESIGN.md §3.1.
 //
-//   groups   G_1 = tile bits [0,K) (contiguous tiles; "A"), then high groups
-//            of <= K - m_min target qubits each, tile = 2^m contiguous runs.
+//   groups   G_1 = "A" = tile amp bits [0, KA) (one contiguous run per tile),
+//            then high groups "H" of <= KA - MA target qubits each; an H tile
+//            is 2^(KA-MA) runs of 2^MA contiguous amplitudes.
 //   order    the mixer qubits of one layer commute, so layer k visits the
 //            groups forward or backward ("ping-pong"); the last group of
 //            layer k is the first of layer k+1 and one sweep does
 //            mix_k(X) -> phase_{k+1} -> mix_{k+1}(X).  The last layer ends on
 //            G_1 so the final reductions see contiguous tiles (sampler CDF).
-//   passes   1 + p*(S-1) HBM round trips for S groups (first one write-only)
-//            versus n + p(E_n + n) in the reference's per-gate engine.
+//   passes   1 + p*(S-1) HBM round trips for S >= 2 groups (the first one is
+//            write-only) versus n + p(E_n + n) in the reference's per-gate engine.
+//   rounds   the register layouts of each sweep are fixed at compile time per
+//            (group kind, sweep kind) (lrq_sweep.cuh prog_*); the planner only
+//            assigns which register bits take a butterfly in which round.
 #pragma once
 #include <stdint.h>
 
 #include <string>
 #include <vector>
 
+#include "lrq_sweep.cuh"
+
 namespace lrq {
 
-struct PlanRound {
-  int lo;
-  unsigned m1, m2;
-  bool phase, reduce;
-};
-
 struct PlanGroup {
-  int m, q0;          // tile map
-  unsigned tmask;     // tile bits that are mixer targets
-  std::vector<int> layouts;  // register layouts, first one I/O capable
+  int kind;        // GK_A / GK_H
+  int m, q0;       // tile amp bit i -> global i < m ? i : q0 + (i - m)
+  unsigned tmask;  // tile amp bits that are mixer targets
   int ntargets;
 };
 
 struct PlanSweep {
   int group;
-  bool init, store;
-  int beta1, beta2;   // layer index of mixer 1 / 2 (-1: none)
-  int phase;          // layer index of the cost phase (-1: none)
+  int kind;                 // SK_*
+  int beta1, phase, beta2;  // layer indices (-1: none)
   bool reduce;
-  std::vector<PlanRound> rounds;
-  int store_lo;
+  int nrounds;
+  unsigned mask1[kMaxRounds], mask2[kMaxRounds];  // register-amp-bit masks
+  unsigned tmask1[kMaxRounds], tmask2[kMaxRounds];  // same, as tile amp bits
 };
 
 struct Plan {
-  int n, K, RB, NTB;
-  bool small;  // n < K: whole-state kernel
+  int n, KA, pair;
+  bool small;  // n < KA: whole-state kernel
   std::vector<PlanGroup> groups;
   std::vector<PlanSweep> sweeps;
 };
 
-inline bool plan_io_ok(const PlanGroup& g, int lo, int RB) {
-  if (!(lo >= g.m || lo + RB <= g.m)) return false;  // register bits on one side of m
-  return lo >= 3 || g.m <= lo;                        // lanes cover >= 8 contiguous amplitudes
-}
-
-inline std::vector<PlanGroup> plan_groups(int n, int K, int RB, int kmax) {
+inline std::vector<PlanGroup> plan_groups(int n, int pair) {
+  const int KA = kUnitBits + pair;
   std::vector<PlanGroup> gs;
   PlanGroup a;
-  a.m = K;
-  a.q0 = K;
-  a.tmask = (K >= 32) ? 0xffffffffu : ((1u << K) - 1u);
-  a.ntargets = K;
-  // first layout: top register block (I/O capable); then 0, RB, 2RB, ...
-  a.layouts.push_back(K - RB);
-  for (int lo = 0; lo < K - RB; lo += RB) a.layouts.push_back(lo);
+  a.kind = GK_A;
+  a.m = KA;
+  a.q0 = KA;
+  a.tmask = (1u << KA) - 1u;
+  a.ntargets = KA;
   gs.push_back(a);
-  for (int g0 = K; g0 < n; g0 += kmax) {
+  // high groups: as few as possible; for complex64 as many of them as the
+  // count allows use 128 B runs (H4, 9 targets), the rest 64 B runs (H, 10)
+  const int rest = n > KA ? n - KA : 0;
+  const int kH = KA - group_ma(GK_H, pair);
+  const int nh = (rest + kH - 1) / kH;
+  int n_h4 = 0;
+  if (pair) {
+    const int kH4 = KA - group_ma(GK_H4, pair);
+    const int need10 = rest - kH4 * nh;  // groups that must take 10 targets
+    n_h4 = nh - (need10 > 0 ? need10 : 0);
+  }
+  for (int i = 0, g0 = KA; g0 < n; ++i) {
+    const int kind = i < n_h4 ? GK_H4 : GK_H;
+    const int MA = group_ma(kind, pair);
+    const int kmax = KA - MA;
     const int k = (n - g0) < kmax ? (n - g0) : kmax;
-    const int kk = k > RB ? k : RB;
     PlanGroup h;
-    h.m = K - kk;
-    h.q0 = (k >= RB) ? g0 : g0 + k - RB;
+    h.kind = kind;
+    h.m = MA;
+    h.q0 = g0 + k - kmax;  // short last group: slide the run down (extra bits are non-targets)
     h.tmask = 0;
-    for (int i = h.m; i < K; ++i) {
-      const int gp = h.q0 + (i - h.m);
+    for (int i = MA; i < KA; ++i) {
+      const int gp = h.q0 + (i - MA);
       if (gp >= g0 && gp < g0 + k) h.tmask |= 1u << i;
     }
     h.ntargets = k;
-    for (int lo = K - RB; lo > h.m; lo -= RB) h.layouts.push_back(lo);
-    if (h.layouts.empty() || h.layouts.back() != h.m) {
-      // last layout starts at m (may overlap the previous one)
-      bool covered = true;
-      unsigned cov = 0;
-      for (int lo : h.layouts) cov |= ((1u << RB) - 1u) << lo;
-      if ((cov & h.tmask) != h.tmask) covered = false;
-      if (!covered) h.layouts.push_back(h.m);
-    }
     gs.push_back(h);
+    g0 += k;
   }
   return gs;
 }
 
-// greedy assignment of target bits to the rounds of one traversal
-inline std::vector<unsigned> plan_masks(const PlanGroup& g, const std::vector<int>& order, int RB) {
-  std::vector<unsigned> out;
-  unsigned rem = g.tmask;
-  for (int lo : order) {
-    const unsigned reg = ((1u << RB) - 1u) << lo;
-    const unsigned take = rem & reg;
-    rem &= ~take;
-    out.push_back(take >> lo);
+// Butterfly masks come from the compile-time programs (prog_mask); a masked
+// register bit that is not one of the group's targets gets tangent 0.
+// mask*[r] = register amp bits that take a real butterfly in round r,
+// tmask*[r] = the same bits as tile amp bits.
+inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
+  const int RA = 4 + pair;
+  sw.nrounds = prog_rounds(g.kind, pair, sw.kind);
+  for (int r = 0; r < sw.nrounds; ++r) {
+    const int lo = prog_lo(g.kind, pair, sw.kind, r);
+    const unsigned pm[2] = {prog_mask(g.kind, pair, sw.kind, r, 0), prog_mask(g.kind, pair, sw.kind, r, 1)};
+    unsigned m[2] = {0, 0}, tm[2] = {0, 0};
+    for (int w = 0; w < 2; ++w)
+      for (int a = 0; a < RA; ++a) {
+        const unsigned tb = 1u << reg_tile_bit(pair, lo, a);
+        if (((pm[w] >> a) & 1u) && (g.tmask & tb)) {
+          m[w] |= 1u << a;
+          tm[w] |= tb;
+        }
+      }
+    sw.mask1[r] = sw.beta1 >= 0 ? m[0] : 0;
+    sw.mask2[r] = sw.beta2 >= 0 ? m[1] : 0;
+    sw.tmask1[r] = sw.beta1 >= 0 ? tm[0] : 0;
+    sw.tmask2[r] = sw.beta2 >= 0 ? tm[1] : 0;
   }
-  return out;
 }
 
-inline Plan make_plan(int n, int NTB, int RB, int p, int kmax) {
+inline PlanSweep make_sweep(int group, int kind, int b1, int ph, int b2, bool red) {
+  PlanSweep s;
+  s.group = group;
+  s.kind = kind;
+  s.beta1 = b1;
+  s.phase = ph;
+  s.beta2 = b2;
+  s.reduce = red;
+  s.nrounds = 0;
+  for (int r = 0; r < kMaxRounds; ++r) s.mask1[r] = s.mask2[r] = s.tmask1[r] = s.tmask2[r] = 0;
+  return s;
+}
+
+inline Plan make_plan(int n, int pair, int p) {
   Plan P;
   P.n = n;
-  P.NTB = NTB;
-  P.RB = RB;
-  P.K = NTB + RB;
-  P.small = n < P.K;
+  P.pair = pair;
+  P.KA = kUnitBits + pair;
+  P.small = n < P.KA;
   if (P.small || p < 1) return P;
-  P.groups = plan_groups(n, P.K, RB, kmax);
+  P.groups = plan_groups(n, pair);
   const int S = (int)P.groups.size();
-
-  // op stream: INIT, then per layer PHASE_k, MIX_k(g) for g in the layer order
-  struct Op { int kind; int layer; int group; };  // kind 0 phase, 1 mix
-  std::vector<Op> ops;
-  for (int k = 0; k < p; ++k) {
-    ops.push_back({0, k, -1});
-    const bool reversed = ((p - 1 - k) % 2) == 0;  // last layer reversed -> ends on G_1
-    for (int i = 0; i < S; ++i) ops.push_back({1, k, reversed ? S - 1 - i : i});
+  if (S == 1) {
+    P.sweeps.push_back(make_sweep(0, SK_P, -1, 0, 0, false));
+    for (int k = 1; k < p; ++k) P.sweeps.push_back(make_sweep(0, SK_L, -1, k, k, k == p - 1));
+    if (p == 1) P.sweeps.push_back(make_sweep(0, SK_Q, -1, -1, -1, true));
+  } else {
+    // layer k visits groups backward when (p-1-k) is even, so layer p-1 ends on G_1
+    auto order = [&](int k, int i) { return ((p - 1 - k) % 2 == 0) ? S - 1 - i : i; };
+    P.sweeps.push_back(make_sweep(order(0, 0), SK_P, -1, 0, 0, false));
+    for (int k = 0; k < p; ++k) {
+      for (int i = 1; i < S - 1; ++i) P.sweeps.push_back(make_sweep(order(k, i), SK_M, k, -1, -1, false));
+      const int last = order(k, S - 1);
+      if (k + 1 < p) P.sweeps.push_back(make_sweep(last, SK_F, k, k + 1, k + 1, false));
+      else P.sweeps.push_back(make_sweep(last, SK_R, k, -1, -1, true));
+    }
   }
-  // greedy fusion: [init|load] [mix1 X] [phase] [mix2 X] [reduce if last & X==0]
-  size_t i = 0;
-  bool first = true;
-  while (i < ops.size()) {
-    PlanSweep sw;
-    sw.init = first;
-    sw.store = true;
-    sw.beta1 = sw.beta2 = sw.phase = -1;
-    sw.reduce = false;
-    // group of this sweep: the first mix op at or after i
-    size_t j = i;
-    while (j < ops.size() && ops[j].kind != 1) ++j;
-    sw.group = ops[j].group;
-    if (!first && ops[i].kind == 1 && ops[i].group == sw.group) {
-      sw.beta1 = ops[i].layer;
-      ++i;
-    }
-    if (i < ops.size() && ops[i].kind == 0) {
-      sw.phase = ops[i].layer;
-      ++i;
-      if (i < ops.size() && ops[i].kind == 1 && ops[i].group == sw.group) {
-        sw.beta2 = ops[i].layer;
-        ++i;
-      }
-    }
-    if (i == ops.size()) sw.reduce = true;  // planner guarantees group 0 here
-    first = false;
-
-    const PlanGroup& g = P.groups[sw.group];
-    const std::vector<int>& L = g.layouts;
-    std::vector<int> fwd(L.begin(), L.end()), rev(L.rbegin(), L.rend());
-    if (sw.beta1 >= 0 && sw.beta2 >= 0) {
-      std::vector<unsigned> a = plan_masks(g, fwd, RB), b = plan_masks(g, rev, RB);
-      for (size_t r = 0; r < fwd.size(); ++r) sw.rounds.push_back({fwd[r], a[r], 0u, false, false});
-      sw.rounds.back().phase = true;
-      sw.rounds.back().m2 = b[0];
-      for (size_t r = 1; r < rev.size(); ++r) sw.rounds.push_back({rev[r], 0u, b[r], false, false});
-    } else if (sw.beta1 >= 0) {
-      std::vector<unsigned> a = plan_masks(g, fwd, RB);
-      for (size_t r = 0; r < fwd.size(); ++r) sw.rounds.push_back({fwd[r], a[r], 0u, false, false});
-    } else {
-      // [init|load] phase mix2 : phase in the last layout, mix2 backwards
-      std::vector<unsigned> b = plan_masks(g, rev, RB);
-      for (size_t r = 0; r < rev.size(); ++r)
-        sw.rounds.push_back({rev[r], 0u, sw.beta2 >= 0 ? b[r] : 0u, false, false});
-      sw.rounds.front().phase = sw.phase >= 0;
-    }
-    if (sw.reduce) sw.rounds.back().reduce = true;
-    const int last = sw.rounds.back().lo;
-    sw.store_lo = plan_io_ok(g, last, RB) ? last : L.front();
-    P.sweeps.push_back(sw);
-  }
+  for (PlanSweep& s : P.sweeps) plan_rounds(P.groups[s.group], pair, s);
   return P;
 }
 
 inline std::string plan_json(const Plan& P) {
-  std::string s = "{\"n\":" + std::to_string(P.n) + ",\"K\":" + std::to_string(P.K) +
-                  ",\"RB\":" + std::to_string(P.RB) + ",\"small\":" + (P.small ? "true" : "false") +
-                  ",\"groups\":[";
+  static const char* kinds = "PMFRLQN";
+  std::string s = "{\"n\":" + std::to_string(P.n) + ",\"K\":" + std::to_string(P.KA) + ",\"pair\":" +
+                  std::to_string(P.pair) + ",\"small\":" + (P.small ? "true" : "false") + ",\"groups\":[";
   for (size_t i = 0; i < P.groups.size(); ++i) {
     const PlanGroup& g = P.groups[i];
     s += (i ? "," : "");
-    s += "{\"m\":" + std::to_string(g.m) + ",\"q0\":" + std::to_string(g.q0) + ",\"tmask\":" +
-         std::to_string(g.tmask) + ",\"layouts\":[";
-    for (size_t j = 0; j < g.layouts.size(); ++j) s += (j ? "," : "") + std::to_string(g.layouts[j]);
-    s += "]}";
+    s += "{\"kind\":\"" + std::string(g.kind == GK_A ? "A" : (g.kind == GK_H4 ? "H4" : "H")) + "\",\"m\":" + std::to_string(g.m) +
+         ",\"q0\":" + std::to_string(g.q0) + ",\"tmask\":" + std::to_string(g.tmask) + "}";
   }
   s += "],\"sweeps\":[";
   for (size_t i = 0; i < P.sweeps.size(); ++i) {
     const PlanSweep& w = P.sweeps[i];
+    const PlanGroup& g = P.groups[w.group];
     s += (i ? "," : "");
-    s += "{\"group\":" + std::to_string(w.group) + ",\"init\":" + (w.init ? "true" : "false") +
-         ",\"beta1\":" + std::to_string(w.beta1) + ",\"phase\":" + std::to_string(w.phase) +
-         ",\"beta2\":" + std::to_string(w.beta2) + ",\"reduce\":" + (w.reduce ? "true" : "false") +
-         ",\"store_lo\":" + std::to_string(w.store_lo) + ",\"rounds\":[";
-    for (size_t r = 0; r < w.rounds.size(); ++r) {
-      const PlanRound& R = w.rounds[r];
+    s += "{\"group\":" + std::to_string(w.group) + ",\"kind\":\"" + kinds[w.kind] + "\",\"init\":" +
+         (w.kind == SK_P ? "true" : "false") + ",\"beta1\":" + std::to_string(w.beta1) +
+         ",\"phase\":" + std::to_string(w.phase) + ",\"beta2\":" + std::to_string(w.beta2) +
+         ",\"reduce\":" + (w.reduce ? "true" : "false") + ",\"rounds\":[";
+    for (int r = 0; r < w.nrounds; ++r) {
       s += (r ? "," : "");
-      s += "[" + std::to_string(R.lo) + "," + std::to_string(R.m1) + "," + std::to_string(R.m2) + "," +
-           (R.phase ? "1" : "0") + "," + (R.reduce ? "1" : "0") + "]";
+      s += "[" + std::to_string(prog_lo(g.kind, P.pair, w.kind, r)) + "," + std::to_string(w.tmask1[r]) + "," +
+           std::to_string(w.tmask2[r]) + "," + (prog_phase(w.kind, g.kind, P.pair, r) ? "1" : "0") + "," +
+           (prog_reduce(w.kind, g.kind, P.pair, r) ? "1" : "0") + "]";
     }
     s += "]}";
   }

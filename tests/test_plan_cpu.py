@@ -104,7 +104,7 @@ def test_plan_emulation_matches_oracle(lib, n, p, pb):
     mixer = np.array([-b for b in betas])  # RX(theta=-2 beta): half angle -beta
     if n > 20:  # emulation only (oracle too slow): check structure
         S = len(plan["groups"])
-        assert len(plan["sweeps"]) == 1 + p * (S - 1) if S > 1 else p
+        assert len(plan["sweeps"]) == (1 + p * (S - 1) if S > 1 else p + (p == 1))
         return
     got = emulate(plan, n, phase, mixer)
     want = O.simulate(n, w, p, "fp64")
@@ -117,7 +117,6 @@ def test_plan_structure(lib, n, pb):
     for p in (1, 2, 3, 10):
         plan = json.loads(_native.describe_plan(n, pb, p))
         K = plan["K"]
-        RB = plan["RB"]
         if n < K:
             assert plan["small"]
             continue
@@ -129,22 +128,28 @@ def test_plan_structure(lib, n, pb):
         assert sorted(cover) == list(range(n))
         S = len(groups)
         sweeps = plan["sweeps"]
-        assert len(sweeps) == (1 + p * (S - 1) if S > 1 else p)
+        assert len(sweeps) == (1 + p * (S - 1) if S > 1 else p + (p == 1))
         assert sweeps[0]["init"] and sweeps[0]["phase"] == 0
         assert sweeps[-1]["reduce"] and sweeps[-1]["group"] == 0
+        pair = plan["pair"]
         for sw in sweeps:
             g = groups[sw["group"]]
             m1 = m2 = 0
             for lo, a, b, _, _ in sw["rounds"]:
-                assert 0 <= lo <= K - RB
-                m1 |= a << lo
-                m2 |= b << lo
+                assert lo in (0, 2, 3, 4, 8)
+                assert not (m1 & a) and not (m2 & b), "a target takes one butterfly per mixer"
+                m1 |= a
+                m2 |= b
             if sw["beta1"] >= 0:
                 assert m1 == g["tmask"]
             if sw["beta2"] >= 0:
                 assert m2 == g["tmask"]
-            # global I/O layouts keep register bits on one side of m
-            for lo in {sw["store_lo"], sw["rounds"][0][0]}:
-                assert lo >= g["m"] or lo + RB <= g["m"]
+            # global I/O layouts: lanes walk contiguous units (never the lo=0
+            # layout of group A; H layouts keep register units above the run)
+            for lo in {sw["rounds"][-1][0], sw["rounds"][0][0]}:
+                if g["kind"] == "A":
+                    assert lo != 0
+                else:
+                    assert lo >= g["m"] - pair
         if n in (32,) and pb == 8:
             assert S == 3  # 2 HBM passes per layer for the bench workload
