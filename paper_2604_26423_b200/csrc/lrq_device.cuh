@@ -103,6 +103,11 @@ __device__ __forceinline__ float2 conj32(float2 a) { return make_float2(a.x, -a.
 // streaming global access (each amplitude is read once and written once per
 // sweep; the state is far larger than L2, so mark it evict-first)
 
+// TMA bulk prefetch of [p, p+bytes) into L2 (bytes: multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ float4 ld_unit(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_unit(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_unit(float4* p, float4 v) { __stcs(p, v); }

@@ -209,6 +209,41 @@ void fill_tangents(SweepParams& sp, int w, const unsigned* masks, int nrounds, d
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// Tensor map over the runs of an H-group tile, in 8-byte elements:
+//   d0 = run (2^MA amps), d1 = block bits below q0, d2/d3 = run index bits
+//   (strides 2^q0 amps), d4 = block bits above the run index.
+bool make_run_tmap(CUtensorMap* tm, void* amps, int n, int pbytes, int MA, int KA, int q0) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const int ea = pbytes / 8, nrb = KA - MA, r1 = nrb < 5 ? nrb : 5;
+  const cuuint64_t B = (cuuint64_t)pbytes;
+  cuuint64_t dims[5] = {(cuuint64_t)(1u << MA) * ea, 1ull << (q0 - MA), 1ull << r1, 1ull << (nrb - r1),
+                        1ull << (n - q0 - nrb)};
+  cuuint64_t strides[4] = {(1ull << MA) * B, (1ull << q0) * B, (1ull << (q0 + r1)) * B, (1ull << (q0 + nrb)) * B};
+  cuuint32_t box[5] = {(cuuint32_t)dims[0], 1, (cuuint32_t)dims[2], (cuuint32_t)dims[3], 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void cpow_mul(double& re, double& im, double qre, double qim, int k) {
   for (int i = 0; i < k; ++i) {
     const double r = re * qre - im * qim, m = re * qim + im * qre;

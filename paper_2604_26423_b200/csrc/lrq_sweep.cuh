@@ -22,6 +22,8 @@
 // A layout "lo" puts tile unit bits [lo, lo+4) in registers; the thread index
 // fills the remaining 8 unit bits in ascending order.
 #pragma once
+#include <cuda.h>
+
 #include "lrq_device.cuh"
 
 namespace lrq {
@@ -120,6 +122,10 @@ struct MatArg {
 };
 
 struct SweepParams {
+  // H groups: 5-D tensor map over the tile's 2^(KA-MA) runs, used to prefetch
+  // a CTA's next tile into L2 with one TMA instruction (has_tmap = 0: none)
+  CUtensorMap tmap;
+  int has_tmap;
   void* amps;
   int n;   // local amp bits
   int q0;  // global amp bit of tile amp bit MA (group A: KA)

@@ -236,7 +236,7 @@ struct SweepTile {
 };
 
 template <typename T, int GK, int SK>
-__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepParams P) {
+__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepParams P) {
   typedef SweepCtx<T, GK, SK> S;
   typedef SweepTile<T, GK, SK> W;
   typedef typename S::U U;
@@ -337,6 +337,24 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const SweepParams P)
       const int sh = S::gshift(LO, qU);
 #pragma unroll
       for (int j = 0; j < 16; ++j) c.r[j] = ld_unit(g + ((uint64_t)j << sh));
+      // group A: pull this CTA's next (contiguous, 64 KB) tile into L2 with one
+      // TMA bulk prefetch while the current one is computed.  (For the strided
+      // H tiles the 2^(12-MU) small prefetches cost more than they hide.)
+      if (t == 0) {
+        const long long nxt = tid + gridDim.x;
+        if constexpr (GK == GK_A) {
+          if (nxt < P.num_tiles) prefetch_l2(gamps + ((uint64_t)nxt << kUnitBits), 16u << kUnitBits);
+        } else {
+          // one TMA tensor prefetch covers all 2^(12-MU) strided runs of the tile
+          if (P.has_tmap && nxt < P.num_tiles) {
+            const int c1 = (int)((uint64_t)nxt & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)nxt >> bl);
+            asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&P.tmap)),
+                         "r"(0), "r"(c1), "r"(0), "r"(0), "r"(c4)
+                         : "memory");
+          }
+        }
+      }
       if (!HAS_PHASE && !(P.scale_re == 1.0 && P.scale_im == 0.0)) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
