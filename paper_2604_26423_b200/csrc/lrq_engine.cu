@@ -14,7 +14,7 @@
 #include "../../include/lrq.h"
 #include "lrq_aux.cuh"
 #include "lrq_plan.h"
-#include "lrq_sweep_kernel.cuh"
+#include "lrq_sweep_tma.cuh"
 
 using namespace lrq;
 
@@ -40,6 +40,11 @@ int fail(int code, const std::string& msg) {
 // amplitudes (pair = 1 for complex64: a unit holds two amplitudes)
 inline int pair_of(int pbytes) { return pbytes == 8 ? 1 : 0; }
 inline int tile_amp_bits(int pbytes) { return kUnitBits + pair_of(pbytes); }
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
 
 template <typename T, int GK, int SK>
 int launch_sweep_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
@@ -229,6 +234,45 @@ EncodeTiledFn encode_tiled() {
 // Tensor map over the runs of an H-group tile, in 8-byte elements:
 //   d0 = run (2^MA amps), d1 = block bits below q0, d2/d3 = run index bits
 //   (strides 2^q0 amps), d4 = block bits above the run index.
+// Tensor map whose box is one whole 64 KB tile in natural tile order, with
+// the 128B swizzle the TMA sweep kernel reads (8-byte elements):
+//   A (contiguous):  {16, 256, 2T} box {16, 256, 2}
+//   H complex64:     {2^MA, 32 runs, 2^(q0-MA) block, 2^(nrb-5) runs, rest} box {2^MA, 32, 1, 2^(nrb-5), 1}
+//   H complex128:    {16, 2, 2^(q0-4) block, 256 runs, rest}            box {16, 2, 1, 256, 1}
+// Coordinates of tile tid: A (0, 0, 2 tid); H (0, 0, tid_low, 0, tid_high).
+bool make_tile_tmap(CUtensorMap* tm, void* amps, int gk, int n, int pbytes, int MA, int KA, int q0,
+                    long long num_tiles) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t B = (cuuint64_t)pbytes;
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  if (gk == GK_A) {
+    cuuint64_t dims[3] = {16, 256, 2ull * (cuuint64_t)num_tiles};
+    cuuint64_t strides[2] = {128, 32768};
+    cuuint32_t box[3] = {16, 256, 2};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  const int nrb = KA - MA;
+  if (pbytes == 8) {
+    // 64 B runs (MA = 3) use the 64B swizzle: a swizzled box row is padded
+    // to the swizzle width, so 64 B rows under the 128B mode would not fit
+    cuuint64_t dims[5] = {1ull << MA, 32, 1ull << (q0 - MA), 1ull << (nrb - 5), 1ull << (n - q0 - nrb)};
+    cuuint64_t strides[4] = {(1ull << q0) * B, (1ull << MA) * B, (1ull << (q0 + 5)) * B, (1ull << (q0 + nrb)) * B};
+    cuuint32_t box[5] = {(cuuint32_t)(1u << MA), 32, 1, (cuuint32_t)(1u << (nrb - 5)), 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              MA == 3 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  cuuint64_t dims[5] = {16, 2, 1ull << (q0 - MA), 1ull << nrb, 1ull << (n - q0 - nrb)};
+  cuuint64_t strides[4] = {128, (1ull << MA) * B, (1ull << q0) * B, (1ull << (q0 + nrb)) * B};
+  cuuint32_t box[5] = {16, 2, 1, (cuuint32_t)(1u << nrb), 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_run_tmap(CUtensorMap* tm, void* amps, int n, int pbytes, int MA, int KA, int q0) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
@@ -252,13 +296,89 @@ void cpow_mul(double& re, double& im, double qre, double qim, int k) {
   }
 }
 
-int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp, int grid) {
+template <typename T, int GK, int SK, int TEAMS>
+int launch_tma_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(sweep_tma_kernel<T, GK, SK, TEAMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024);
+  });
+  CUDA_TRY(err);
+  sweep_tma_kernel<T, GK, SK, TEAMS><<<grid, TEAMS * kThreads, smem, st>>>(sp);
+  CUDA_TRY(cudaGetLastError());
+  return LRQ_OK;
+}
+
+template <typename T, int GK, int TEAMS>
+int launch_tma_kind(cudaStream_t st, int sk, const SweepParams& sp, int grid, size_t smem) {
+  switch (sk) {
+    case SK_M: return launch_tma_t<T, GK, SK_M, TEAMS>(st, sp, grid, smem);
+    case SK_F: return launch_tma_t<T, GK, SK_F, TEAMS>(st, sp, grid, smem);
+  }
+  if constexpr (GK == GK_A) {
+    switch (sk) {
+      case SK_R: return launch_tma_t<T, GK, SK_R, TEAMS>(st, sp, grid, smem);
+      case SK_L: return launch_tma_t<T, GK, SK_L, TEAMS>(st, sp, grid, smem);
+      case SK_Q: return launch_tma_t<T, GK, SK_Q, TEAMS>(st, sp, grid, smem);
+    }
+  }
+  return fail(LRQ_ERUNTIME, "internal: no TMA sweep kernel for this (group, kind)");
+}
+
+template <typename T, int TEAMS>
+int launch_tma_any(cudaStream_t st, int gk, int sk, const SweepParams& sp, int grid, size_t smem) {
+  if (gk == GK_A) return launch_tma_kind<T, GK_A, TEAMS>(st, sk, sp, grid, smem);
+  if (gk == GK_H) return launch_tma_kind<T, GK_H, TEAMS>(st, sk, sp, grid, smem);
+  if constexpr (sizeof(T) == 4) return launch_tma_kind<T, GK_H4, TEAMS>(st, sk, sp, grid, smem);
+  return fail(LRQ_ERUNTIME, "internal: no complex128 H4 group");
+}
+
+// Which sweeps take the TMA-fed pipeline: $LRQ_SWEEP_PATH = "reg" (none),
+// "tma" (all that load), or a list of "<precision><group><kind>" tokens; the
+// default keeps each sweep on the path measured faster on B200
+// (profiles/r01_*): complex64 M and F on high groups.
+bool use_tma_path(int pbytes, int gk, int sk) {
+  if (sk == SK_P || sk == SK_N) return false;
+  const char* v = getenv("LRQ_SWEEP_PATH");
+  if (v && strcmp(v, "reg") == 0) return false;
+  if (v && strcmp(v, "tma") == 0) return true;
+  const char* g = gk == GK_A ? "A" : (gk == GK_H4 ? "H4" : "H");
+  char tok[16];
+  snprintf(tok, sizeof tok, "%s%s%c", pbytes == 8 ? "c64" : "c128", g, "PMFRLQN"[sk]);
+  if (v && *v) return strstr(v, tok) != nullptr;
+  return pbytes == 8 && gk != GK_A && (sk == SK_M || sk == SK_F);
+}
+
+int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int grid) {
   const bool amps = sk != SK_N;
   const bool usesJ = sk == SK_P || sk == SK_F || sk == SK_L;
-  const bool usesW = sk == SK_R || sk == SK_Q || sk == SK_N || (sk == SK_L && sp.reduce);
-  const size_t smem = sweep_smem_bytes(sp.n, amps, usesJ, usesW);
-  if (s->pbytes == 8) return launch_sweep_kind<float>(s->stream, gk, sk, sp, grid, smem);
-  return launch_sweep_kind<double>(s->stream, gk, sk, sp, grid, smem);
+  const bool usesW = sk == SK_R || sk == SK_Q || sk == SK_N || (sk == SK_L && sp_in.reduce);
+  if (use_tma_path(s->pbytes, gk, sk)) {
+    // TMA-fed pipeline: one CTA per SM, a ring of 64 KB stages, 1 or 2 teams
+    SweepParams sp = sp_in;
+    const int K = tile_amp_bits(s->pbytes);
+    const int ma = group_ma(gk, pair_of(s->pbytes));
+    if (!make_tile_tmap(&sp.tmap, s->amps, gk, sp.n, s->pbytes, ma, K, sp.q0, s->num_tiles))
+      return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
+    sp.has_tmap = 1;
+    const size_t cap = 227 * 1024;
+    int teams = env_int("LRQ_TMA_TEAMS", 1);  // 2 teams measured no faster (profiles/r01_*)
+    teams = teams == 1 ? 1 : 2;
+    if (teams == 2 && tma_smem_bytes(sp.n, 3, 2, usesJ, usesW) > cap) teams = 1;
+    sp.nstages = tma_smem_bytes(sp.n, 3, teams, usesJ, usesW) <= cap ? 3 : 2;
+    const size_t smem = tma_smem_bytes(sp.n, sp.nstages, teams, usesJ, usesW);
+    const int sms = sm_count(s->device);
+    const int g = (int)(s->num_tiles < sms ? s->num_tiles : sms);
+    if (s->pbytes == 8)
+      return teams == 2 ? launch_tma_any<float, 2>(s->stream, gk, sk, sp, g, smem)
+                        : launch_tma_any<float, 1>(s->stream, gk, sk, sp, g, smem);
+    return teams == 2 ? launch_tma_any<double, 2>(s->stream, gk, sk, sp, g, smem)
+                      : launch_tma_any<double, 1>(s->stream, gk, sk, sp, g, smem);
+  }
+  const size_t smem = sweep_smem_bytes(sp_in.n, amps, usesJ, usesW);
+  if (s->pbytes == 8) return launch_sweep_kind<float>(s->stream, gk, sk, sp_in, grid, smem);
+  return launch_sweep_kind<double>(s->stream, gk, sk, sp_in, grid, smem);
 }
 
 template <typename T>

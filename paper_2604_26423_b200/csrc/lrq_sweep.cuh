@@ -126,6 +126,7 @@ struct SweepParams {
   // a CTA's next tile into L2 with one TMA instruction (has_tmap = 0: none)
   CUtensorMap tmap;
   int has_tmap;
+  int nstages;  // TMA path: shared-memory stages in the load ring (2 or 3)
   void* amps;
   int n;   // local amp bits
   int q0;  // global amp bit of tile amp bit MA (group A: KA)
@@ -256,8 +257,8 @@ struct SweepCtx {
   // per-tile field on every tile bit from the tile's fixed bits (warp w0) and
   // the fixed bits' own energy (warp w0+1)
   __device__ static void block_consts(const double* M, const double* X, double cst, int n, int q0, uint64_t base,
-                                      int w0, double* hb, double* ebb) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                      int w0, double* hb, double* ebb, int tl) {
+    const int warp = tl >> 5, lane = tl & 31;  // tl: thread index within the 256-thread team
     if (warp == w0) {
       if (lane < KA) {
         const int gi = gpos(lane, q0);

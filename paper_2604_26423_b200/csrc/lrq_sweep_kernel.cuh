@@ -23,7 +23,8 @@ struct SweepTile {
     U r[16];
     const SweepParams* P;
     U* tile;
-    const double* thr;  // per-thread constants [mat][6][kThreads]
+    const double* thr;   // per-thread constants of the phase matrix [6][kThreads]
+    const double* thrW;  // per-thread constants of the cost matrix [6][kThreads]
     const double* hbJ;  // per-tile fields (phase matrix)
     const double* hbW;  // per-tile fields (cost matrix)
     double ebbJ, ebbW;
@@ -34,6 +35,7 @@ struct SweepTile {
     uint64_t base;  // amp index of tile element 0
     long long tid;
     int t, q0, qU;
+    int bar;  // named barrier of this 256-thread team
   };
 
   // complex64: the angles are assembled and reduced mod 2pi in float64, the
@@ -119,7 +121,7 @@ struct SweepTile {
 
   __device__ static __forceinline__ void reduce(Ctx& c, int lo) {
     const SweepParams& P = *c.P;
-    const double* th = c.thr + 6 * kThreads;
+    const double* th = c.thrW;
     double F[RA];
     double C = c.ebbW + th[RA * kThreads + c.t];
     bool thread_ok = true;
@@ -186,7 +188,7 @@ struct SweepTile {
       c.rs[warp * 4 + 2] = mine;
       c.rs[warp * 4 + 3] = __longlong_as_double((long long)zbest);
     }
-    __syncthreads();
+    team_sync(c.bar);  // the 256 threads of this team only
     if (c.t == 0) {
       double s0 = 0.0, s1 = 0.0, mn = c.rs[2];
       unsigned long long zb = (unsigned long long)__double_as_longlong(c.rs[3]);
@@ -304,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   c.P = &P;
   c.tile = tile;
   c.thr = thr;
+  c.thrW = thr + 6 * kThreads;
   c.PRR = PRR;
   c.PRR32 = PRR32;
   c.ERR = ERR;
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   c.t = t;
   c.q0 = q0;
   c.qU = qU;
+  c.bar = 1;
   U* gamps = reinterpret_cast<U*>(P.amps);
   const int bl = qU - MU;  // block unit bits below the high run
 
@@ -322,8 +326,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     c.tid = tid;
     double* hbJ = hB + (par * 2 + 0) * 16;
     double* hbW = hB + (par * 2 + 1) * 16;
-    if (HAS_PHASE) S::block_consts(Jm, Jx, P.J.cst, n, q0, c.base, 0, hbJ, &EBB[par * 2 + 0]);
-    if (usesW) S::block_consts(Wm, Wx, P.W.cst, n, q0, c.base, 2, hbW, &EBB[par * 2 + 1]);
+    if (HAS_PHASE) S::block_consts(Jm, Jx, P.J.cst, n, q0, c.base, 0, hbJ, &EBB[par * 2 + 0], t);
+    if (usesW) S::block_consts(Wm, Wx, P.W.cst, n, q0, c.base, 2, hbW, &EBB[par * 2 + 1], t);
     __syncthreads();
     c.hbJ = hbJ;
     c.hbW = hbW;
