@@ -475,10 +475,14 @@ int lrq_create(int n, int pbytes, int device, uint64_t budget, lrq_state** out) 
   if (e == cudaSuccess) e = cudaMalloc(&s->red, sizeof(double) * 4 * s->num_tiles);
   if (e == cudaSuccess) e = cudaMalloc(&s->prefix, sizeof(double) * (s->num_tiles + 1));
   if (e == cudaSuccess) e = cudaMalloc(&s->out, sizeof(double) * 4);
+  // zero-fills on the engine's own (non-blocking) stream and waited for: a
+  // legacy-stream cudaMemset is not ordered with it and could land after the
+  // first lrq_set_cost copy
   if (e == cudaSuccess) e = cudaMalloc(&s->dW, sizeof(double) * n * n);
-  if (e == cudaSuccess) e = cudaMemset(s->dW, 0, sizeof(double) * n * n);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->dW, 0, sizeof(double) * n * n, s->stream);
   if (e == cudaSuccess) e = cudaMalloc(&s->dzero, sizeof(double) * (n + 1));
-  if (e == cudaSuccess) e = cudaMemset(s->dzero, 0, sizeof(double) * (n + 1));
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->dzero, 0, sizeof(double) * (n + 1), s->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) {
     free_state(s);
     return fail(e == cudaErrorMemoryAllocation ? LRQ_ECAPACITY : LRQ_ERUNTIME,
