@@ -93,6 +93,24 @@ int lrq_cut_values(int num_qubits, const double *w, const uint64_t *z, uint64_t 
  * device: lowest-index argmax of C; value re-evaluated bit-exactly.         */
 int lrq_max_cut(int num_qubits, const double *w, int device, uint64_t *argmax, double *value);
 
+/* multi-GPU (one process per GPU) — replaces the shard threads of
+ * run_circuit_sharded (sharded.py:202-385).  world = 2^g ranks; rank r holds
+ * the 2^(n-g) amplitudes whose top g bits equal r.  All ranks call lrq_run,
+ * lrq_reduce and lrq_sample collectively (NCCL inside); lrq_sample returns
+ * the same global indices on every rank; lrq_copy_amps reads the local shard.
+ * nccl_id: 128 bytes from lrq_nccl_unique_id on one rank, shared by the host. */
+int lrq_nccl_unique_id(void *out, size_t cap);
+int lrq_create_dist(int num_qubits, int precision_bytes, int device, int rank, int world, const void *nccl_id,
+                    uint64_t memory_budget, lrq_state **out);
+int lrq_dist_info(lrq_state *s, int *n_local, int *rank, int *world);
+
+/* Host-only helpers of the distributed plan (CPU-testable): the JSON sweep /
+ * remap schedule, and a rank's local view of a Z-Z coupling (lexicographic
+ * edges) in permutation state perm: local matrix, field, constant.          */
+int lrq_describe_dist_plan(int num_qubits, int log2_world, int precision_bytes, int p, char *buf, size_t cap);
+int lrq_dist_terms(int num_qubits, int log2_world, int rank, int perm, const double *edges, double *local_matrix,
+                   double *field, double *constant);
+
 /* timing: per-launch device milliseconds of the last lrq_run (CUDA events on
  * the engine stream), plus the engine stream handle for external events.   */
 int lrq_set_timing(lrq_state *s, int enable);

@@ -51,6 +51,11 @@ _SIGNATURES = {
     "lrq_get_timings": ([_state_p, _p, ctypes.c_char_p, _c_int, ctypes.POINTER(_c_int)], _c_int),
     "lrq_stream": ([_state_p, ctypes.POINTER(_p)], _c_int),
     "lrq_synchronize": ([_state_p], _c_int),
+    "lrq_nccl_unique_id": ([_p, ctypes.c_size_t], _c_int),
+    "lrq_create_dist": ([_c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_u64, ctypes.POINTER(_state_p)], _c_int),
+    "lrq_dist_info": ([_state_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
+    "lrq_describe_dist_plan": ([_c_int, _c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
+    "lrq_dist_terms": ([_c_int, _c_int, _c_int, _c_int, _p, _p, _p, ctypes.POINTER(_c_dbl)], _c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -109,6 +114,30 @@ def ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
+def describe_dist_plan(n: int, log2_world: int, precision_bytes: int, p: int) -> str:
+    buf = ctypes.create_string_buffer(1 << 20)
+    check(lib().lrq_describe_dist_plan(n, log2_world, precision_bytes, p, buf, len(buf)))
+    return buf.value.decode()
+
+
+def dist_terms(n: int, log2_world: int, rank: int, perm: int, edges: np.ndarray):
+    """A rank's local view (matrix, field, constant) of a lexicographic Z-Z
+    coupling in permutation state perm (host-only; see lrq_dist.cuh)."""
+    edges = np.ascontiguousarray(edges, dtype=np.float64)
+    nl = n - log2_world
+    m = np.empty((nl, nl))
+    f = np.empty(nl)
+    c = _c_dbl(0.0)
+    check(lib().lrq_dist_terms(n, log2_world, rank, perm, ptr(edges), ptr(m), ptr(f), ctypes.byref(c)))
+    return m, f, float(c.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().lrq_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
 # One parked lrq_state per (n, precision, device): run_circuit in a loop then
 # reuses the HBM allocation instead of cudaFree/cudaMalloc of the whole state.
 _POOL: dict = {}
@@ -139,13 +168,37 @@ class DeviceState:
         check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
         self._h = h
 
+    @classmethod
+    def create_dist(cls, n: int, precision_bytes: int, device: int, rank: int, world: int, nccl_id: bytes,
+                    budget: int = 0) -> "DeviceState":
+        """One rank's shard of a state distributed over `world` GPUs (collective:
+        every rank calls this with the same nccl_id)."""
+        self = cls.__new__(cls)
+        self._h = None
+        self.n = n
+        self.precision_bytes = precision_bytes
+        self.device = int(device)
+        h = _state_p()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128)
+        check(lib().lrq_create_dist(n, precision_bytes, self.device, rank, world, idbuf, int(budget),
+                                    ctypes.byref(h)))
+        self._h = h
+        self._dist = True
+        return self
+
+    def close(self, park: bool = True) -> None:
+        """Release the state (distributed shards are never parked)."""
+        if getattr(self, "_dist", False):
+            park = False
+        self._close(park)
+
     @property
     def handle(self):
         if self._h is None:
             raise StateError("device state has been released")
         return self._h
 
-    def close(self, park: bool = True) -> None:
+    def _close(self, park: bool = True) -> None:
         """Release the state; the allocation is parked for reuse unless the
         pool already holds one for this shape (or park=False)."""
         if self._h is not None and _lib is not None:

@@ -186,20 +186,28 @@ __global__ void __launch_bounds__(1024) finalize_kernel(long long T, const doubl
 // whose normalised cumulative probability exceeds u).  One warp per shot:
 // binary search over tile prefixes, then an in-tile scan in index order.
 template <typename T>
+// Multi-GPU: this shard's CDF starts at goff of a global mass gtotal; it owns
+// the uniforms in [goff, goff + its mass) / gtotal and writes 0 for the rest
+// (the ranks' outputs are then summed); indices get the rank bits base_index.
 __global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tiles, const double* __restrict__ prefix,
-                              const double* __restrict__ u, long long shots, unsigned long long* __restrict__ out) {
+                              const double* __restrict__ u, long long shots, double goff, double gtotal,
+                              unsigned long long base_index, unsigned long long* __restrict__ out) {
   typedef typename CxT<T>::V V;
   const V* amps = reinterpret_cast<const V*>(amps_);
   const int lane = threadIdx.x & 31;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (warp >= shots) return;
-  const double total = prefix[T_tiles];
+  const double total = gtotal;
   const double x = u[warp];
-  // first tile b with prefix[b+1] / total > x
+  if (!(goff / total <= x && (goff + prefix[T_tiles]) / total > x)) {
+    if (lane == 0) out[warp] = 0ull;
+    return;
+  }
+  // first tile b with (goff + prefix[b+1]) / total > x
   long long lo = 0, hi = T_tiles - 1;
   while (lo < hi) {
     const long long mid = (lo + hi) >> 1;
-    if (prefix[mid + 1] / total > x) hi = mid;
+    if ((goff + prefix[mid + 1]) / total > x) hi = mid;
     else lo = mid + 1;
   }
   const long long b = lo;
@@ -216,13 +224,13 @@ __global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tile
     const double y = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += y;
   }
-  const double off = prefix[b];
+  const double off = goff + prefix[b];
   const bool hit = e0 < L && (off + inc) / total > x;
   const unsigned ballot = __ballot_sync(0xffffffffu, hit);
   long long idx;
   if (ballot == 0) {
     idx = (b << tile_bits) + L - 1;
-    if (lane == 0) out[warp] = (unsigned long long)idx;
+    if (lane == 0) out[warp] = base_index + (unsigned long long)idx;
     return;
   }
   const int L0 = __ffs(ballot) - 1;
@@ -236,7 +244,7 @@ __global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tile
         break;
       }
     }
-    out[warp] = (unsigned long long)((b << tile_bits) + idx);
+    out[warp] = base_index + (unsigned long long)((b << tile_bits) + idx);
   }
 }
 

@@ -14,6 +14,7 @@
 #include "../../include/lrq.h"
 #include "lrq_aux.cuh"
 #include "lrq_plan.h"
+#include "lrq_dist.cuh"
 #include "lrq_sweep_tma.cuh"
 
 using namespace lrq;
@@ -138,6 +139,17 @@ struct lrq_state {
   std::vector<cudaEvent_t> evs;
   std::vector<char> kinds;
   std::vector<double> last_ms;
+  // distributed (world > 1): n above is the local qubit count n_total - g
+  int world = 1, rank = 0, g = 0, n_total = 0;
+  ncclComm_t comm = nullptr;
+  unsigned char* stage = nullptr;  // remap staging, (world-1) * chunk bytes
+  size_t chunk = 0;
+  std::vector<double> cost_edges;  // global cost edges (lexicographic)
+  double* dWx = nullptr;           // cost field from the rank's qubits (n_loc)
+  double wcst = 0.0;
+  double* dgather = nullptr;       // 4 * world doubles (all-gathered reductions)
+  std::vector<double> rank_sum_p;  // per-rank probability mass of the last run
+  double remap_ms = 0.0;
 };
 
 namespace {
@@ -155,6 +167,10 @@ void free_state(lrq_state* s) {
   cudaFree(s->dmix);
   cudaFree(s->du);
   cudaFree(s->didx);
+  cudaFree(s->stage);
+  cudaFree(s->dWx);
+  cudaFree(s->dgather);
+  if (s->comm && nccl().ok) nccl().CommDestroy(s->comm);
   for (cudaEvent_t e : s->evs) cudaEventDestroy(e);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -270,21 +286,6 @@ bool make_tile_tmap(CUtensorMap* tm, void* amps, int gk, int n, int pbytes, int 
   cuuint32_t box[5] = {16, 2, 1, (cuuint32_t)(1u << nrb), 1};
   return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-bool make_run_tmap(CUtensorMap* tm, void* amps, int n, int pbytes, int MA, int KA, int q0) {
-  EncodeTiledFn fn = encode_tiled();
-  if (!fn) return false;
-  const int ea = pbytes / 8, nrb = KA - MA, r1 = nrb < 5 ? nrb : 5;
-  const cuuint64_t B = (cuuint64_t)pbytes;
-  cuuint64_t dims[5] = {(cuuint64_t)(1u << MA) * ea, 1ull << (q0 - MA), 1ull << r1, 1ull << (nrb - r1),
-                        1ull << (n - q0 - nrb)};
-  cuuint64_t strides[4] = {(1ull << MA) * B, (1ull << q0) * B, (1ull << (q0 + r1)) * B, (1ull << (q0 + nrb)) * B};
-  cuuint32_t box[5] = {(cuuint32_t)dims[0], 1, (cuuint32_t)dims[2], (cuuint32_t)dims[3], 1};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -410,9 +411,209 @@ void record(lrq_state* s, size_t idx, char kind) {
   if (kind) s->kinds.push_back(kind);
 }
 
+#define NCCL_TRY(expr)                                                                           \
+  do {                                                                                           \
+    ncclResult_t r_ = (expr);                                                                    \
+    if (r_ != ncclSuccess)                                                                       \
+      return fail(LRQ_ERUNTIME, std::string("NCCL error in ") + #expr + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+// Exchange, chunk by chunk, local block `b` (top g local bits = b) with
+// rank `b`'s block `rank`: the all-to-all block transpose that swaps the g
+// global qubits with the top g local qubits.  peer >= 0: instead swap the
+// whole local state with that one rank (used by the deferred global flip).
+int exchange_blocks(lrq_state* s, int peer) {
+  NcclApi& nc = nccl();
+  const size_t block = peer >= 0 ? (size_t)s->pbytes << s->n : (size_t)s->pbytes << (s->n - s->g);
+  unsigned char* base = reinterpret_cast<unsigned char*>(s->amps);
+  for (size_t off = 0; off < block; off += s->chunk) {
+    const size_t len = block - off < s->chunk ? block - off : s->chunk;
+    NCCL_TRY(nc.GroupStart());
+    int slot = 0;
+    for (int b = 0; b < s->world; ++b) {
+      if (b == s->rank || (peer >= 0 && b != peer)) continue;
+      const size_t at = (peer >= 0 ? 0 : (size_t)b * block) + off;
+      NCCL_TRY(nc.Send(base + at, len, ncclUint8, b, s->comm, s->stream));
+      NCCL_TRY(nc.Recv(s->stage + (size_t)slot * s->chunk, len, ncclUint8, b, s->comm, s->stream));
+      ++slot;
+    }
+    NCCL_TRY(nc.GroupEnd());
+    slot = 0;
+    for (int b = 0; b < s->world; ++b) {
+      if (b == s->rank || (peer >= 0 && b != peer)) continue;
+      const size_t at = (peer >= 0 ? 0 : (size_t)b * block) + off;
+      CUDA_TRY(cudaMemcpyAsync(base + at, s->stage + (size_t)slot * s->chunk, len, cudaMemcpyDeviceToDevice,
+                               s->stream));
+      ++slot;
+    }
+  }
+  return LRQ_OK;
+}
+
+// lrq_run for world > 1 (make_dist_plan): local sweeps in the permutation
+// state each one records, remaps between layers, final read-only reduction.
+int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
+  const int nl = s->n, nt = s->n_total, g = s->g, E = nt * (nt - 1) / 2;
+  const size_t per = (size_t)nl * nl + nl;
+  if (2 * p > s->jcap) {
+    cudaFree(s->dJ);
+    s->dJ = nullptr;
+    CUDA_TRY(cudaMalloc(&s->dJ, sizeof(double) * per * 2 * p));
+    s->jcap = 2 * p;
+  }
+  std::vector<double> J(per * 2 * p), cst(2 * p);
+  for (int k = 0; k < p; ++k)
+    for (int perm = 0; perm < 2; ++perm) {
+      double* dst = J.data() + per * (2 * k + perm);
+      dist_terms(nt, g, s->rank, perm, phase + (size_t)k * E, dst, dst + (size_t)nl * nl, &cst[2 * k + perm]);
+    }
+  CUDA_TRY(cudaMemcpyAsync(s->dJ, J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice, s->stream));
+  const double init = s->pbytes == 8 ? init_amplitude<float>(nt) : init_amplitude<double>(nt);
+  s->reduced = false;
+  s->ran = false;
+  s->kinds.clear();
+  size_t ev = 0;
+  record(s, ev++, 0);
+  double* rp = s->red;
+  double* rpe = rp + s->num_tiles;
+  double* rmin = rpe + s->num_tiles;
+  unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
+  // the final pass runs in the identity permutation: the top logical qubit is
+  // rank bit g-1 (max-cut search over top bit 0)
+  const int min_bit = ((s->rank >> (g - 1)) & 1) ? -2 : -1;
+  const Plan P = make_dist_plan(nl, g, pair_of(s->pbytes), p);
+  const int grid_cap = 2 * sm_count(s->device);
+  const int grid = (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap);
+  int flips = 0;
+  for (int k = 0; k < p; ++k) flips += mixer_form(mixer[k]).flip;
+  for (const PlanSweep& w : P.sweeps) {
+    const PlanGroup& gr = P.groups[w.group];
+    if (w.kind == SK_Q && (flips & 1)) {
+      // deferred X^(x)n of the flipped layers: z -> ~z reverses the local index
+      // and maps rank r to rank world-1-r
+      const long long half = (1ll << nl) / 2;
+      const unsigned blocks = (unsigned)((half + 255) / 256);
+      if (s->pbytes == 8) reverse_kernel<float2><<<blocks, 256, 0, s->stream>>>(s->amps, nl);
+      else reverse_kernel<double2><<<blocks, 256, 0, s->stream>>>(s->amps, nl);
+      CUDA_TRY(cudaGetLastError());
+      int rc = exchange_blocks(s, s->world - 1 - s->rank);
+      if (rc) return rc;
+      record(s, ev++, 'X');
+    }
+    SweepParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.amps = s->amps;
+    sp.n = nl;
+    sp.q0 = gr.q0;
+    sp.num_tiles = s->num_tiles;
+    sp.reduce = w.reduce ? 1 : 0;
+    double sre = 1.0, sim = 0.0;
+    if (w.beta1 >= 0) {
+      const MixerForm f = mixer_form(mixer[w.beta1]);
+      fill_tangents(sp, 0, w.mask1, w.nrounds, f.t);
+      cpow_mul(sre, sim, f.qre, f.qim, w.ntarget1);
+    }
+    if (w.beta2 >= 0) {
+      const MixerForm f = mixer_form(mixer[w.beta2]);
+      fill_tangents(sp, 1, w.mask2, w.nrounds, f.t);
+      cpow_mul(sre, sim, f.qre, f.qim, w.ntarget2);
+    }
+    sp.scale_re = sre;
+    sp.scale_im = sim;
+    sp.init_re = init;
+    const double* jm = w.phase >= 0 ? s->dJ + per * (2 * w.phase + w.perm) : s->dW;
+    sp.J.M = jm;
+    sp.J.ext = w.phase >= 0 ? jm + (size_t)nl * nl : s->dzero;
+    sp.J.cst = w.phase >= 0 ? cst[2 * w.phase + w.perm] : 0.0;
+    sp.W.M = s->dW;
+    sp.W.ext = s->dWx;
+    sp.W.cst = s->wcst;
+    sp.min_bit = min_bit;
+    sp.red_p = rp;
+    sp.red_pE = rpe;
+    sp.red_minE = rmin;
+    sp.red_arg = rarg;
+    int rc = launch_sweep(s, gr.kind, w.kind, sp, grid);
+    if (rc) return rc;
+    record(s, ev++, "PMFRLQN"[w.kind]);
+    if (w.remap_after) {
+      rc = exchange_blocks(s, -1);
+      if (rc) return rc;
+      record(s, ev++, 'T');
+    }
+  }
+  finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
+  CUDA_TRY(cudaGetLastError());
+  record(s, ev++, 'Z');
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->timing) {
+    s->last_ms.clear();
+    for (size_t i = 1; i < ev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, s->evs[i - 1], s->evs[i]);
+      s->last_ms.push_back(ms);
+    }
+  }
+  s->ran = true;
+  s->reduced = true;
+  s->rank_sum_p.clear();
+  return LRQ_OK;
+}
+
+// all ranks: the per-rank finalize scalars, gathered in rank order
+int gather_out(lrq_state* s, std::vector<double>& h) {
+  NCCL_TRY(nccl().AllGather(s->out, s->dgather, 4, ncclDouble, s->comm, s->stream));
+  h.resize(4 * s->world);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), s->dgather, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return LRQ_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int lrq_nccl_unique_id(void* out, size_t cap) {
+  if (!out || cap < sizeof(ncclUniqueId)) return fail(LRQ_EVALIDATION, "unique-id buffer too small");
+  NcclApi& nc = nccl();
+  if (!nc.ok) return fail(LRQ_ERUNTIME, nc.err);
+  ncclUniqueId id;
+  NCCL_TRY(nc.GetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return LRQ_OK;
+}
+
+int lrq_dist_terms(int n, int g, int rank, int perm, const double* edges, double* mloc, double* ext,
+                   double* cst) {
+  if (n < 2 || g < 0 || g >= n || !edges || !mloc || !ext || !cst) return fail(LRQ_EVALIDATION, "bad argument");
+  if (rank < 0 || rank >= (1 << g)) return fail(LRQ_EVALIDATION, "rank out of range");
+  dist_terms(n, g, rank, perm, edges, mloc, ext, cst);
+  return LRQ_OK;
+}
+
+int lrq_describe_dist_plan(int n, int g, int pbytes, int p, char* buf, size_t cap) {
+  if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
+  if (g < 1 || g > 6) return fail(LRQ_EVALIDATION, "log2(world) out of range [1, 6]");
+  if (p < 1) return fail(LRQ_EVALIDATION, "p must be >= 1");
+  const int nl = n - g, KA = tile_amp_bits(pbytes);
+  if (nl <= KA) return fail(LRQ_EVALIDATION, "distributed engine needs n - log2(world) > " + std::to_string(KA));
+  const Plan P = make_dist_plan(nl, g, pair_of(pbytes), p);
+  if (P.groups.back().ntargets < g)
+    return fail(LRQ_EVALIDATION, "last qubit group smaller than log2(world); choose another n");
+  std::string js = plan_json(P);
+  // append the distributed fields per sweep: [perm, remap_after, target1]
+  js.pop_back();
+  js += ",\"dist\":[";
+  for (size_t i = 0; i < P.sweeps.size(); ++i) {
+    const PlanSweep& w = P.sweeps[i];
+    js += (i ? "," : "");
+    js += "[" + std::to_string(w.perm) + "," + (w.remap_after ? "1" : "0") + "," + std::to_string(w.target1) + "]";
+  }
+  js += "]}";
+  if (!buf || cap < js.size() + 1) return fail(LRQ_EVALIDATION, "buffer too small: need " + std::to_string(js.size() + 1));
+  memcpy(buf, js.c_str(), js.size() + 1);
+  return LRQ_OK;
+}
 
 int lrq_abi_version(void) { return LRQ_ABI_VERSION; }
 
@@ -497,17 +698,79 @@ int lrq_destroy(lrq_state* s) {
   return LRQ_OK;
 }
 
+int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, const void* nccl_id,
+                    uint64_t memory_budget, lrq_state** out) {
+  if (!out || !nccl_id) return fail(LRQ_EVALIDATION, "null argument");
+  *out = nullptr;
+  if (world < 2 || (world & (world - 1))) return fail(LRQ_EVALIDATION, "world size must be a power of two >= 2");
+  if (rank < 0 || rank >= world) return fail(LRQ_EVALIDATION, "rank out of range");
+  if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
+  int g = 0;
+  while ((1 << g) < world) ++g;
+  const int nl = n_total - g, KA = tile_amp_bits(pbytes);
+  if (nl <= KA) return fail(LRQ_EVALIDATION, "distributed engine needs n - log2(world) > " + std::to_string(KA));
+  if (plan_groups(nl, pair_of(pbytes)).back().ntargets < g)
+    return fail(LRQ_EVALIDATION, "last qubit group smaller than log2(world); choose another n");
+  NcclApi& nc = nccl();
+  if (!nc.ok) return fail(LRQ_ERUNTIME, nc.err);
+  lrq_state* s = nullptr;
+  int rc = lrq_create(nl, pbytes, device, memory_budget, &s);
+  if (rc) return rc;
+  s->world = world;
+  s->rank = rank;
+  s->g = g;
+  s->n_total = n_total;
+  DeviceGuard guard(device);
+  const size_t block = (size_t)pbytes << (nl - g);
+  s->chunk = block < (64ull << 20) ? block : (64ull << 20);
+  cudaError_t e = cudaMalloc(&s->stage, s->chunk * (size_t)(world - 1));
+  if (e == cudaSuccess) e = cudaMalloc(&s->dWx, sizeof(double) * nl);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->dWx, 0, sizeof(double) * nl, s->stream);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * 4 * world);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) {
+    free_state(s);
+    return fail(LRQ_ECAPACITY, std::string("distributed buffers: ") + cudaGetErrorString(e));
+  }
+  ncclUniqueId id;
+  memcpy(&id, nccl_id, sizeof id);
+  ncclResult_t r = nc.CommInitRank(&s->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    s->comm = nullptr;
+    free_state(s);
+    return fail(LRQ_ERUNTIME, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
+  }
+  *out = s;
+  return LRQ_OK;
+}
+
+int lrq_dist_info(lrq_state* s, int* n_local, int* rank, int* world) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (n_local) *n_local = s->n;
+  if (rank) *rank = s->rank;
+  if (world) *world = s->world;
+  return LRQ_OK;
+}
+
 int lrq_set_cost(lrq_state* s, const double* w) {
   if (!s || !w) return fail(LRQ_EVALIDATION, "null argument");
-  const int n = s->n, E = n * (n - 1) / 2;
+  const int n = s->n, nt = s->world > 1 ? s->n_total : s->n, E = nt * (nt - 1) / 2;
   std::vector<double> M((size_t)n * n);
   double tot = 0.0;
   for (int e = 0; e < E; ++e) {
     if (!isfinite(w[e])) return fail(LRQ_EVALIDATION, "edge weight is not finite");
     tot += w[e];
   }
-  sym_matrix(n, w, M.data());
   DeviceGuard guard(s->device);
+  if (s->world > 1) {
+    // local view in the identity permutation (the final pass runs there)
+    std::vector<double> ext(n);
+    s->cost_edges.assign(w, w + E);
+    dist_terms(nt, s->g, s->rank, 0, w, M.data(), ext.data(), &s->wcst);
+    CUDA_TRY(cudaMemcpyAsync(s->dWx, ext.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+  } else {
+    sym_matrix(n, w, M.data());
+  }
   CUDA_TRY(cudaMemcpyAsync(s->dW, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->wtot = tot;
@@ -520,12 +783,13 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   if (!s) return fail(LRQ_EVALIDATION, "null state");
   if (p < 1) return fail(LRQ_EVALIDATION, "depth p must be >= 1");
   if (!phase || !mixer) return fail(LRQ_EVALIDATION, "null phase/mixer arrays");
-  const int n = s->n, E = n * (n - 1) / 2;
-  for (long long i = 0; i < (long long)p * E; ++i)
+  const int n = s->n, nt = s->world > 1 ? s->n_total : n, E = n * (n - 1) / 2, Et = nt * (nt - 1) / 2;
+  for (long long i = 0; i < (long long)p * Et; ++i)
     if (!isfinite(phase[i])) return fail(LRQ_EVALIDATION, "phase angle is not finite");
   for (int k = 0; k < p; ++k)
     if (!isfinite(mixer[k])) return fail(LRQ_EVALIDATION, "mixer angle is not finite");
   DeviceGuard guard(s->device);
+  if (s->world > 1) return run_dist(s, p, phase, mixer);
   if (p > s->jcap) {
     cudaFree(s->dJ);
     cudaFree(s->dmix);
@@ -711,6 +975,34 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
   if (!s->reduced) return fail(LRQ_ERUNTIME, "no reductions: set a cost and run the circuit first");
   DeviceGuard guard(s->device);
   double h[4];
+  if (s->world > 1) {
+    // collective: every rank's scalars, combined in rank order (deterministic);
+    // local argmin -> global index (rank bits on top, identity permutation)
+    std::vector<double> all;
+    int rc = gather_out(s, all);
+    if (rc) return rc;
+    double sp = 0.0, spe = 0.0, mn = __builtin_inf();
+    uint64_t best = ~0ull;
+    s->rank_sum_p.assign(s->world, 0.0);
+    for (int r = 0; r < s->world; ++r) {
+      sp += all[4 * r];
+      spe += all[4 * r + 1];
+      s->rank_sum_p[r] = all[4 * r];
+      uint64_t z;
+      memcpy(&z, &all[4 * r + 3], 8);
+      if (z == ~0ull) continue;
+      const uint64_t gz = ((uint64_t)r << s->n) | z;
+      if (all[4 * r + 2] < mn || (all[4 * r + 2] == mn && gz < best)) {
+        mn = all[4 * r + 2];
+        best = gz;
+      }
+    }
+    out->sum_p = sp;
+    out->sum_p_cut = 0.5 * (s->wtot * sp - spe);
+    out->min_energy = mn;
+    out->argmax_cut = best;
+    return LRQ_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(h, s->out, sizeof h, cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   out->sum_p = h[0];
@@ -727,9 +1019,25 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   if (shots < 1) return fail(LRQ_EVALIDATION, "shot count must be positive, got " + std::to_string(shots));
   if (!s->reduced) return fail(LRQ_ERUNTIME, "no CDF: set a cost and run the circuit first");
   DeviceGuard guard(s->device);
-  double total = 0.0;
-  CUDA_TRY(cudaMemcpyAsync(&total, s->out, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  double total = 0.0, off = 0.0;
+  unsigned long long base_index = 0;
+  if (s->world > 1) {
+    // global CDF over ranks in rank order: this rank owns the uniforms that
+    // land in [off, off + its mass) / total
+    if ((int)s->rank_sum_p.size() != s->world) {
+      lrq_reduction tmp;
+      int rc = lrq_reduce(s, &tmp);
+      if (rc) return rc;
+    }
+    for (int r = 0; r < s->world; ++r) {
+      if (r == s->rank) off = total;
+      total += s->rank_sum_p[r];
+    }
+    base_index = (unsigned long long)s->rank << s->n;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(&total, s->out, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
   if (!(total > 0.0)) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
   if (shots > s->shot_cap) {
     cudaFree(s->du);
@@ -747,11 +1055,13 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   const long long grid = (threads + block - 1) / block;
   if (s->pbytes == 8)
     sample_kernel<float><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
-                                                                   shots, s->didx);
+                                                                   shots, off, total, base_index, s->didx);
   else
     sample_kernel<double><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
-                                                                    shots, s->didx);
+                                                                    shots, off, total, base_index, s->didx);
   CUDA_TRY(cudaGetLastError());
+  if (s->world > 1)  // exactly one rank owns each shot; the others wrote 0
+    NCCL_TRY(nccl().AllReduce(s->didx, s->didx, shots, ncclUint64, ncclSum, s->comm, s->stream));
   CUDA_TRY(cudaMemcpyAsync(idx, s->didx, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   return LRQ_OK;

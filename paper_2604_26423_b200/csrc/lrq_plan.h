@@ -39,6 +39,12 @@ struct PlanSweep {
   int nrounds;
   unsigned mask1[kMaxRounds], mask2[kMaxRounds];  // register-amp-bit masks
   unsigned tmask1[kMaxRounds], tmask2[kMaxRounds];  // same, as tile amp bits
+  // distributed plans: the mixer-1 targets of a sweep can be a subset of the
+  // group (the qubits a remap just made local); 0 = the whole group
+  unsigned target1;
+  int ntarget1, ntarget2;  // qubits mixed by mixer 1 / 2 (scale factor powers)
+  bool remap_after;        // distributed plans: a qubit remap follows this sweep
+  int perm;                // permutation state the sweep runs in (0 identity, 1 swapped)
 };
 
 struct Plan {
@@ -97,6 +103,9 @@ inline std::vector<PlanGroup> plan_groups(int n, int pair) {
 inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
   const int RA = 4 + pair;
   sw.nrounds = prog_rounds(g.kind, pair, sw.kind);
+  const unsigned targets[2] = {sw.target1 ? sw.target1 : g.tmask, g.tmask};
+  if (!sw.ntarget1) sw.ntarget1 = sw.target1 ? __builtin_popcount(sw.target1) : g.ntargets;
+  if (!sw.ntarget2) sw.ntarget2 = g.ntargets;
   for (int r = 0; r < sw.nrounds; ++r) {
     const int lo = prog_lo(g.kind, pair, sw.kind, r);
     const unsigned pm[2] = {prog_mask(g.kind, pair, sw.kind, r, 0), prog_mask(g.kind, pair, sw.kind, r, 1)};
@@ -104,7 +113,7 @@ inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
     for (int w = 0; w < 2; ++w)
       for (int a = 0; a < RA; ++a) {
         const unsigned tb = 1u << reg_tile_bit(pair, lo, a);
-        if (((pm[w] >> a) & 1u) && (g.tmask & tb)) {
+        if (((pm[w] >> a) & 1u) && (targets[w] & tb)) {
           m[w] |= 1u << a;
           tm[w] |= tb;
         }
@@ -125,6 +134,10 @@ inline PlanSweep make_sweep(int group, int kind, int b1, int ph, int b2, bool re
   s.beta2 = b2;
   s.reduce = red;
   s.nrounds = 0;
+  s.target1 = 0;
+  s.ntarget1 = s.ntarget2 = 0;
+  s.remap_after = false;
+  s.perm = 0;
   for (int r = 0; r < kMaxRounds; ++r) s.mask1[r] = s.mask2[r] = s.tmask1[r] = s.tmask2[r] = 0;
   return s;
 }
@@ -153,6 +166,61 @@ inline Plan make_plan(int n, int pair, int p) {
       else P.sweeps.push_back(make_sweep(last, SK_R, k, -1, -1, true));
     }
   }
+  for (PlanSweep& s : P.sweeps) plan_rounds(P.groups[s.group], pair, s);
+  return P;
+}
+
+// ---------------------------------------------------------------------------
+// Distributed plan (one process per GPU, G = 2^g ranks, n_loc = n - g local
+// qubits).  Physical bits [0, n_loc) are local, [n_loc, n) are
+// the rank.  The cost phase is fully local (the rank's qubits enter as a field
+// and a constant), the mixer needs every qubit local once per layer: after a
+// layer's local sweeps one remap (all-to-all block transpose) swaps the g
+// global qubits with the top g local bits L' (inside the last group Z), and
+// the next sweep on Z starts with the mixer of the just-arrived qubits:
+//   layer 0:  P(Z) [init, phase_0, mix_0(Z)], M(others) mix_0, REMAP
+//   layer k:  F(Z) [mix_{k-1}(L'), phase_k, mix_k(Z)], M(others) mix_k, REMAP
+//   end:      M(Z) [mix_{p-1}(L')], (REMAP if the permutation is odd), Q(A)
+// Each sweep records the permutation state it runs in (the phase terms
+// depend on it); two remaps restore the identity.
+inline Plan make_dist_plan(int n_loc, int g, int pair, int p) {
+  Plan P;
+  P.n = n_loc;
+  P.pair = pair;
+  P.KA = kUnitBits + pair;
+  P.small = false;
+  P.groups = plan_groups(n_loc, pair);
+  const int S = (int)P.groups.size();
+  const int Z = S - 1;
+  const PlanGroup& gz = P.groups[Z];
+  // tile bits of group Z holding the top g local qubits L'
+  unsigned lmask = 0;
+  for (int i = gz.m; i < P.KA; ++i) {
+    const int gp = gz.q0 + (i - gz.m);
+    if (gp >= n_loc - g && gp < n_loc) lmask |= 1u << i;
+  }
+  int perm = 0;
+  for (int k = 0; k < p; ++k) {
+    PlanSweep z = k == 0 ? make_sweep(Z, SK_P, -1, 0, 0, false) : make_sweep(Z, SK_F, k - 1, k, k, false);
+    if (k > 0) z.target1 = lmask;
+    z.perm = perm;
+    P.sweeps.push_back(z);
+    for (int o = 0; o < Z; ++o) {
+      PlanSweep m = make_sweep(o, SK_M, k, -1, -1, false);
+      m.perm = perm;
+      P.sweeps.push_back(m);
+    }
+    P.sweeps.back().remap_after = true;
+    perm ^= 1;
+  }
+  PlanSweep last = make_sweep(Z, SK_M, p - 1, -1, -1, false);
+  last.target1 = lmask;
+  last.perm = perm;
+  last.remap_after = perm == 1;
+  P.sweeps.push_back(last);
+  PlanSweep q = make_sweep(0, SK_Q, -1, -1, -1, true);
+  q.perm = 0;
+  P.sweeps.push_back(q);
   for (PlanSweep& s : P.sweeps) plan_rounds(P.groups[s.group], pair, s);
   return P;
 }

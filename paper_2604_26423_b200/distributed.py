@@ -1,0 +1,123 @@
+"""Multi-GPU LR-QAOA: one process per GPU (torchrun), NCCL over NVLink.
+
+Replaces the reference's thread-per-shard engine (lrqbench sharded.py:202-385)
+for the hot path: rank r holds the 2^(n-g) amplitudes whose top g = log2(world)
+bits equal r.  The cost phase is local on every rank; the mixer of the g
+global qubits costs one NCCL all-to-all block transpose per layer
+(DESIGN.md §5).  torch.distributed is only the bootstrap (it ships the NCCL
+unique id); all device work is liblrq.so.
+
+    torchrun --nproc-per-node 8 ... :
+        dist.init_process_group("gloo")            # or "nccl"
+        sv = run_circuit_distributed(circ, "fp64")  # collective
+        r = sv.exact_expected_r(inst)               # collective
+        shots = sv.sample(10_000, rng_seed=1)       # collective, same on all ranks
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .circuit import CircuitIR, lower_circuit
+from .engine import Precision, ShotSet, check_memory
+from .errors import StateError, ValidationError
+from .problem import WmcInstance
+from .rng import derive_rng
+
+
+def _world(group):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise StateError("run_circuit_distributed needs an initialised torch.distributed process group")
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+class DistStateVector:
+    """This rank's shard of a distributed state (collective methods)."""
+
+    def __init__(self, num_qubits, precision, dev, rank, world, group, cost):
+        self.num_qubits = num_qubits
+        self._precision = precision
+        self._dev = dev
+        self.rank = rank
+        self.world = world
+        self.n_local = num_qubits - (world.bit_length() - 1)
+        self._group = group
+        self._cost = cost
+
+    @property
+    def precision(self) -> Precision:
+        return self._precision
+
+    @property
+    def device_state(self) -> _native.DeviceState:
+        return self._dev
+
+    def reduce(self):
+        return self._dev.reduce()
+
+    def norm_squared(self) -> float:
+        return float(self.reduce().sum_p)
+
+    def exact_expected_r(self, inst: WmcInstance) -> float:
+        if inst.num_vertices != self.num_qubits:
+            raise ValidationError(
+                f"instance has {inst.num_vertices} vertices, state has {self.num_qubits} qubits")
+        if inst.optimal_cut is None:
+            raise StateError("instance has no optimal cut; solve it first")
+        w = inst.weights()
+        if self._cost is None or not np.array_equal(self._cost, w):
+            raise ValidationError("the distributed final pass was fused with another cost; "
+                                  "build the circuit from this instance")
+        return float(self.reduce().sum_p_cut) / inst.optimal_cut.value
+
+    def sample(self, n_shots: int, rng_seed: int) -> ShotSet:
+        if n_shots < 1:
+            raise ValidationError(f"shot count must be positive, got {n_shots}")
+        u = derive_rng(rng_seed, "shots", 0).random(n_shots)
+        return ShotSet(self.num_qubits, self._dev.sample(u), int(rng_seed), "noiseless")
+
+    def local_amps(self) -> np.ndarray:
+        return self._dev.copy_amps()
+
+    def gather_amps(self):
+        """Full state on rank 0 (None elsewhere); small n only."""
+        import torch
+        import torch.distributed as dist
+
+        local = torch.from_numpy(self.local_amps().view(np.float64 if self._precision is Precision.FP64
+                                                        else np.float32).copy())
+        parts = [torch.empty_like(local) for _ in range(self.world)] if self.rank == 0 else None
+        dist.gather(local, parts, dst=0, group=self._group)
+        if self.rank != 0:
+            return None
+        dt = np.complex128 if self._precision is Precision.FP64 else np.complex64
+        return np.concatenate([p.numpy().view(dt) for p in parts])
+
+    def release(self) -> None:
+        self._dev.close()
+
+
+def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Precision.FP32, group=None,
+                            device: int | None = None, memory_budget: int | None = None) -> DistStateVector:
+    """Collective run of an LR-QAOA circuit over all ranks of `group`."""
+    import torch.distributed as dist
+
+    precision = Precision.coerce(precision)
+    rank, world = _world(group)
+    if world & (world - 1):
+        raise ValidationError(f"world size must be a power of two, got {world}")
+    n = circuit.num_qubits
+    g = world.bit_length() - 1
+    check_memory(n - g, precision, memory_budget)
+    layers = lower_circuit(circuit)
+    box = [_native.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    dev_index = _native.default_device() if device is None else int(device)
+    dev = _native.DeviceState.create_dist(n, precision.bytes_per_amplitude, dev_index, rank, world, box[0],
+                                          int(memory_budget or 0))
+    cost = getattr(circuit, "cost_weights", None)
+    dev.set_cost(cost if cost is not None else np.zeros(n * (n - 1) // 2))
+    dev.run(layers.phase, layers.mixer)
+    return DistStateVector(n, precision, dev, rank, world, group, cost)

@@ -1,0 +1,183 @@
+"""CPU tests of the multi-GPU path's host logic with world_size 2 and 4 (gloo).
+
+Each rank runs in its own process and executes the *distributed plan* that
+liblrq.so generates (lrq_describe_dist_plan: sweeps, permutation states,
+remap points, partial mixer targets) on a numpy shard, with the rank's phase
+and cost terms from lrq_dist_terms, remaps as gloo send/recv block
+transposes, and the sampler's rank-partitioned inverse CDF.  The gathered
+state, <C> and the sampled indices must match the CPU oracle.  This checks
+everything of the distributed engine except the kernels themselves (which
+the GPU tests check on one device).
+"""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import lrq_oracle as O
+from paper_2604_26423_b200 import _native
+
+
+def _rx(state, q, h):
+    v = state.reshape(-1, 2, 1 << q)
+    a0 = v[:, 0, :].copy()
+    a1 = v[:, 1, :].copy()
+    c, s = np.cos(h), -1j * np.sin(h)
+    v[:, 0, :] = c * a0 + s * a1
+    v[:, 1, :] = s * a0 + c * a1
+
+
+def _local_energy(nl, m, f, c):
+    z = np.arange(1 << nl, dtype=np.uint64)
+    s = 1.0 - 2.0 * ((z[:, None] >> np.arange(nl, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.float64)
+    return 0.5 * np.einsum("zi,ij,zj->z", s, m, s) + s @ f + c
+
+
+def _exchange(state, rank, world, g):
+    """All-to-all block transpose: local block b (top g local bits) <-> rank b's block `rank`."""
+    nl = int(np.log2(state.size))
+    blocks = state.reshape(world, 1 << (nl - g)).copy()
+    out = blocks.copy()
+    for b in range(world):
+        if b == rank:
+            continue
+        send = torch.from_numpy(blocks[b].view(np.float64).copy())
+        recv = torch.empty_like(send)
+        # lower rank sends first: a fixed order avoids deadlock
+        if rank < b:
+            dist.send(send, b)
+            dist.recv(recv, b)
+        else:
+            dist.recv(recv, b)
+            dist.send(send, b)
+        out[b] = recv.numpy().view(np.complex128)
+    return out.reshape(-1)
+
+
+def _worker(rank, world, port, n, p, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = world.bit_length() - 1
+        nl = n - g
+        plan = json.loads(_native.describe_dist_plan(n, g, 16, p))
+        K = plan["K"]
+        w = O.instance_weights(n, seed)
+        betas, gammas = O.ramp(p)
+        state = np.full(1 << nl, O.uniform_amplitude(n, "fp64"), dtype=np.complex128)
+        remaps = 0
+        for sw, (perm, remap_after, target1) in zip(plan["sweeps"], plan["dist"]):
+            gr = plan["groups"][sw["group"]]
+            phys = lambda i: i if i < gr["m"] else gr["q0"] + i - gr["m"]  # noqa: E731
+            all_t = [phys(i) for i in range(K) if (gr["tmask"] >> i) & 1]
+            t1 = [phys(i) for i in range(K) if (target1 >> i) & 1] if target1 else all_t
+            if sw["beta1"] >= 0:
+                for qb in t1:
+                    _rx(state, qb, -betas[sw["beta1"]])
+            if sw["phase"] >= 0:
+                m, f, c = _native.dist_terms(n, g, rank, perm, gammas[sw["phase"]] * w)
+                state *= np.exp(-1j * _local_energy(nl, m, f, c))
+            if sw["beta2"] >= 0:
+                for qb in all_t:
+                    _rx(state, qb, -betas[sw["beta2"]])
+            if remap_after:
+                state = _exchange(state, rank, world, g)
+                remaps += 1
+        # final pass (identity permutation): sum p, sum p C on this shard
+        m, f, c = _native.dist_terms(n, g, rank, 0, w)
+        cut = 0.5 * (float(w.sum()) - _local_energy(nl, m, f, c))
+        probs = (state.real ** 2 + state.imag ** 2)
+        sums = torch.tensor([probs.sum(), probs @ cut], dtype=torch.float64)
+        parts = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, sums)
+        # sampler: rank-partitioned inverse CDF (lrq_sample / sample_kernel)
+        mass = [float(x[0]) for x in parts]
+        total = sum(mass)
+        off = sum(mass[:rank])
+        u = O.shot_uniforms(1, 2000)
+        cum = off + np.cumsum(probs)
+        idx = np.zeros(u.size, dtype=np.int64)
+        for k, x in enumerate(u):
+            if off / total <= x < (off + probs.sum()) / total:
+                j = int(np.searchsorted(cum / total, x, side="right"))
+                idx[k] = (rank << nl) + min(j, probs.size - 1)
+        shots = torch.from_numpy(idx)
+        dist.all_reduce(shots)
+        gathered = [torch.zeros(2 << nl, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(state.view(np.float64).copy()))
+        if rank == 0:
+            full = np.concatenate([t.numpy().view(np.complex128) for t in gathered])
+            q.put((full, float(sum(x[1] for x in parts)), shots.numpy(), remaps))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2604_26423_b200.build import build
+
+    build()
+
+
+@pytest.mark.parametrize("world,n,p", [(2, 16, 3), (4, 17, 2), (2, 17, 4)])
+def test_distributed_plan_emulation_matches_oracle(world, n, p):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = mp.start_processes(_worker, args=(world, _free_port(), n, p, 3, q), nprocs=world, join=False,
+                               start_method="spawn")
+    full, sum_pc, shots, remaps = q.get()  # before join: the result may exceed the pipe buffer
+    procs.join()
+    w = O.instance_weights(n, 3)
+    want = O.simulate(n, w, p, "fp64")
+    assert np.linalg.norm(full - want) / np.linalg.norm(want) < 1e-12
+    probs = O.probabilities(want)
+    assert sum_pc == pytest.approx(O.expected_cut(n, w, probs), rel=1e-12)
+    ref = O.draw(probs, O.shot_uniforms(1, 2000))
+    assert int(np.sum(shots.astype(np.uint64) != ref)) <= 1
+    assert remaps == p + (p % 2)  # one per layer, plus a restoring one if p is odd
+
+
+def test_dist_terms_reproduce_global_energy():
+    """The local matrix + field + constant of every rank, in both permutation
+    states, reproduce E(z) = sum w s_i s_j of the global index."""
+    n, g = 9, 2
+    w = O.instance_weights(n, 4)
+    z = np.arange(1 << n, dtype=np.uint64)
+    s = 1.0 - 2.0 * ((z[:, None] >> np.arange(n, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.float64)
+    full = O.weight_matrix(n, w)
+    e_glob = 0.5 * np.einsum("zi,ij,zj->z", s, full, s)
+    nl = n - g
+    for perm in (0, 1):
+        for rank in range(1 << g):
+            m, f, c = _native.dist_terms(n, g, rank, perm, w)
+            loc = _local_energy(nl, m, f, c)
+            # physical (rank, local) -> logical index under the permutation
+            for lz in range(1 << nl):
+                bits = [(lz >> k) & 1 for k in range(nl)] + [(rank >> k) & 1 for k in range(g)]
+                if perm:
+                    bits[nl - g:nl], bits[nl:] = bits[nl:], bits[nl - g:nl]
+                zz = sum(b << k for k, b in enumerate(bits))
+                assert abs(loc[lz] - e_glob[zz]) < 1e-12
+
+
+def test_dist_plan_validation():
+    with pytest.raises(Exception):
+        _native.describe_dist_plan(13, 1, 8, 2)  # n_local must exceed the tile
+    plan = json.loads(_native.describe_dist_plan(36, 3, 16, 3))
+    kinds = [s["kind"] for s in plan["sweeps"]]
+    assert kinds[0] == "P" and kinds[-1] == "Q"
+    assert sum(r for _, r, _ in plan["dist"]) == 4  # 3 layer remaps + 1 restoring
