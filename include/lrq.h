@@ -69,6 +69,14 @@ int lrq_set_cost(lrq_state *s, const double *w);
  * set) the fused final pass.  Synchronous.                                  */
 int lrq_run(lrq_state *s, int p, const double *phase, const double *mixer);
 
+/* lrq_run with, per layer k, extra diagonal terms in the cost phase:
+ *   exp(-i (sum_e phase[k*E+e] Z_i Z_j + sum_i field[k*n+i] Z_i + constant[k])).
+ * Single-GPU.  The reference circuits (H, RZZ, RX; circuit.py:66-81) never
+ * need it; it is the single-device form of the rank-local terms the
+ * multi-GPU engine derives from the global qubits (lrq_dist_terms).        */
+int lrq_run_fields(lrq_state *s, int p, const double *phase, const double *field, const double *constant,
+                   const double *mixer);
+
 /* reductions of the last run (exact_expected_r numerator, engine.py:214-226;
  * exhaustive max cut argmax, problem.py:174-211).                            */
 int lrq_reduce(lrq_state *s, lrq_reduction *out);
@@ -103,6 +111,21 @@ int lrq_nccl_unique_id(void *out, size_t cap);
 int lrq_create_dist(int num_qubits, int precision_bytes, int device, int rank, int world, const void *nccl_id,
                     uint64_t memory_budget, lrq_state **out);
 int lrq_dist_info(lrq_state *s, int *n_local, int *rank, int *world);
+
+/* in-process shards — the B200 form of the reference's thread-per-shard
+ * engine (run_circuit_sharded / _ShardWorker, sharded.py:200-385): `world`
+ * shard states in ONE process, one host thread per shard making the same
+ * collective calls as above (lrq_run, lrq_reduce, lrq_sample).  The shards
+ * may share a device or sit on several (peer access).  The group replaces
+ * NCCL with a host barrier and device-side block swaps; a failure in any
+ * collective call aborts the whole group (AbortedRunError, errors.py:24-26).
+ * Destroy the shard states before the group.                               */
+typedef struct lrq_group lrq_group;
+int lrq_group_create(int world, lrq_group **out);
+int lrq_group_destroy(lrq_group *g);
+int lrq_group_abort(lrq_group *g); /* break the group: blocked members return 4 */
+int lrq_create_shard(int num_qubits, int precision_bytes, int device, int rank, lrq_group *g,
+                     uint64_t memory_budget, lrq_state **out);
 
 /* Host-only helpers of the distributed plan (CPU-testable): the JSON sweep /
  * remap schedule, and a rank's local view of a Z-Z coupling (lexicographic

@@ -52,3 +52,19 @@ from .problem import (
     solve_instance,
 )
 from .rng import derive_rng, derive_seed
+from .sharded import (
+    ExchangeStep,
+    GateTiming,
+    ShardedStateVector,
+    ShardPlan,
+    SweepConfig,
+    TimingRecord,
+    exchange_steps,
+    exchange_volume,
+    plan_for_shard_count,
+    plan_shards,
+    remap_volume,
+    run_circuit_sharded,
+    scaling_sweep,
+    write_timing_csv,
+)

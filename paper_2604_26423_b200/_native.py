@@ -41,6 +41,7 @@ _SIGNATURES = {
     "lrq_destroy": ([_state_p], _c_int),
     "lrq_set_cost": ([_state_p, _p], _c_int),
     "lrq_run": ([_state_p, _c_int, _p, _p], _c_int),
+    "lrq_run_fields": ([_state_p, _c_int, _p, _p, _p, _p], _c_int),
     "lrq_reduce": ([_state_p, ctypes.POINTER(Reduction)], _c_int),
     "lrq_recompute": ([_state_p], _c_int),
     "lrq_sample": ([_state_p, _p, _c_i64, _p], _c_int),
@@ -53,6 +54,10 @@ _SIGNATURES = {
     "lrq_synchronize": ([_state_p], _c_int),
     "lrq_nccl_unique_id": ([_p, ctypes.c_size_t], _c_int),
     "lrq_create_dist": ([_c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_u64, ctypes.POINTER(_state_p)], _c_int),
+    "lrq_group_create": ([_c_int, ctypes.POINTER(_p)], _c_int),
+    "lrq_group_destroy": ([_p], _c_int),
+    "lrq_group_abort": ([_p], _c_int),
+    "lrq_create_shard": ([_c_int, _c_int, _c_int, _c_int, _p, _c_u64, ctypes.POINTER(_state_p)], _c_int),
     "lrq_dist_info": ([_state_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
     "lrq_describe_dist_plan": ([_c_int, _c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
     "lrq_dist_terms": ([_c_int, _c_int, _c_int, _c_int, _p, _p, _p, ctypes.POINTER(_c_dbl)], _c_int),
@@ -158,6 +163,7 @@ class DeviceState:
         self.n = n
         self.precision_bytes = precision_bytes
         self.device = default_device() if device is None else int(device)
+        self.n_local = n
         key = (n, precision_bytes, self.device)
         h = _POOL.pop(key, None)
         if h is not None:
@@ -183,6 +189,24 @@ class DeviceState:
         check(lib().lrq_create_dist(n, precision_bytes, self.device, rank, world, idbuf, int(budget),
                                     ctypes.byref(h)))
         self._h = h
+        self.n_local = n - (int(world).bit_length() - 1)
+        self._dist = True
+        return self
+
+    @classmethod
+    def create_shard(cls, n: int, precision_bytes: int, device: int, rank: int, group: "ShardGroup",
+                     budget: int = 0) -> "DeviceState":
+        """Shard `rank` of an in-process shard group (one host thread per shard)."""
+        self = cls.__new__(cls)
+        self._h = None
+        self.n = n
+        self.precision_bytes = precision_bytes
+        self.device = int(device)
+        h = _state_p()
+        check(lib().lrq_create_shard(n, precision_bytes, self.device, rank, group.handle, int(budget),
+                                     ctypes.byref(h)))
+        self._h = h
+        self.n_local = n - (group.world.bit_length() - 1)
         self._dist = True
         return self
 
@@ -225,6 +249,17 @@ class DeviceState:
         mixer = np.ascontiguousarray(mixer, dtype=np.float64)
         check(lib().lrq_run(self.handle, int(mixer.size), ptr(phase), ptr(mixer)))
 
+    def run_fields(self, phase: np.ndarray, field: np.ndarray, constant: np.ndarray, mixer: np.ndarray) -> None:
+        """run() with per-layer single-Z fields (p x n) and constant phases (p)."""
+        phase = np.ascontiguousarray(phase, dtype=np.float64)
+        field = np.ascontiguousarray(field, dtype=np.float64)
+        constant = np.ascontiguousarray(constant, dtype=np.float64)
+        mixer = np.ascontiguousarray(mixer, dtype=np.float64)
+        p = int(mixer.size)
+        if field.size != p * self.n or constant.size != p:
+            raise ValidationError(f"fields need shape ({p}, {self.n}) and constants ({p},)")
+        check(lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
+
     def reduce(self) -> Reduction:
         r = Reduction()
         check(lib().lrq_reduce(self.handle, ctypes.byref(r)))
@@ -241,7 +276,7 @@ class DeviceState:
 
     def copy_amps(self, start: int = 0, count: int | None = None) -> np.ndarray:
         if count is None:
-            count = (1 << self.n) - start
+            count = (1 << self.n_local) - start
         dt = np.complex64 if self.precision_bytes == 8 else np.complex128
         out = np.empty(count, dtype=dt)
         check(lib().lrq_copy_amps(self.handle, start, count, ptr(out)))
@@ -265,6 +300,38 @@ class DeviceState:
 
     def synchronize(self) -> None:
         check(lib().lrq_synchronize(self.handle))
+
+
+class ShardGroup:
+    """Owning handle of an lrq_group (in-process shard transport)."""
+
+    def __init__(self, world: int):
+        h = _p()
+        check(lib().lrq_group_create(int(world), ctypes.byref(h)))
+        self._h = h
+        self.world = int(world)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise StateError("shard group has been released")
+        return self._h
+
+    def abort(self) -> None:
+        """Break the group: members blocked in a collective call return an error."""
+        if self._h is not None:
+            check(lib().lrq_group_abort(self._h))
+
+    def close(self) -> None:
+        if self._h is not None and _lib is not None:
+            check(_lib.lrq_group_destroy(self._h))
+        self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def cut_values(n: int, w: np.ndarray, z: np.ndarray | None = None, start: int = 0, count: int = 0,

@@ -16,6 +16,8 @@ struct SmallParams {
   const double* J;    // p * n * n
   const double* mix;  // p * 2: (cos h, -sin h) of RX(theta), h = theta / 2
   const double* W;    // n * n cost matrix (may be null: no reduction)
+  const double* F;    // p * n single-Z fields (may be null)
+  const double* Fc;   // p constant phases (with F)
   double init_re, init_im;
   int load;  // start from the stored state instead of the init value
   int min_bit;
@@ -49,6 +51,10 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
       double e = 0.0;
       for (int i = 0; i < n; ++i)
         for (int j = i + 1; j < n; ++j) e += J[i * n + j] * spin(z, i) * spin(z, j);
+      if (P.F) {
+        for (int i = 0; i < n; ++i) e += P.F[(size_t)k * n + i] * spin(z, i);
+        e += P.Fc[k];
+      }
       s[z] = cmul_amp(s[z], expmi(e));
     }
     __syncthreads();

@@ -7,6 +7,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -113,6 +115,25 @@ std::string gib(double bytes) {
 
 }  // namespace
 
+// In-process shard group: the shards of one state vector driven by host
+// threads of one process (run_circuit_sharded, sharded.py:202-385), on one or
+// several devices.  It replaces NCCL for these shards: the host barrier
+// orders the streams, and the remap is a device-side swap of the shards'
+// blocks (peer access across devices).  Any failure inside a collective
+// call breaks the group for good (the reference's AbortedRunError).
+struct lrq_group {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int count = 0;
+  unsigned long long gen = 0;
+  bool broken = false;
+  std::string why;
+  std::vector<lrq_state*> members;
+  std::vector<double> gather;               // 4 * world finalize scalars
+  std::vector<const uint64_t*> shot_bufs;  // per-rank host sample buffers
+};
+
 struct lrq_state {
   int n = 0;
   int pbytes = 0;
@@ -142,12 +163,17 @@ struct lrq_state {
   // distributed (world > 1): n above is the local qubit count n_total - g
   int world = 1, rank = 0, g = 0, n_total = 0;
   ncclComm_t comm = nullptr;
+  lrq_group* group = nullptr;      // in-process transport (lrq_create_shard)
   unsigned char* stage = nullptr;  // remap staging, (world-1) * chunk bytes
   size_t chunk = 0;
   std::vector<double> cost_edges;  // global cost edges (lexicographic)
   double* dWx = nullptr;           // cost field from the rank's qubits (n_loc)
   double wcst = 0.0;
   double* dgather = nullptr;       // 4 * world doubles (all-gathered reductions)
+  // optional per-layer Z fields / constant phases (lrq_run_fields)
+  std::vector<double> field_h, cst_h;
+  double* dF = nullptr;
+  int fcap = 0;
   std::vector<double> rank_sum_p;  // per-rank probability mass of the last run
   double remap_ms = 0.0;
 };
@@ -169,8 +195,14 @@ void free_state(lrq_state* s) {
   cudaFree(s->didx);
   cudaFree(s->stage);
   cudaFree(s->dWx);
+  cudaFree(s->dF);
   cudaFree(s->dgather);
   if (s->comm && nccl().ok) nccl().CommDestroy(s->comm);
+  if (s->group) {
+    std::lock_guard<std::mutex> lk(s->group->mu);
+    if (s->rank < (int)s->group->members.size() && s->group->members[s->rank] == s)
+      s->group->members[s->rank] = nullptr;
+  }
   for (cudaEvent_t e : s->evs) cudaEventDestroy(e);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -422,7 +454,103 @@ void record(lrq_state* s, size_t idx, char kind) {
 // rank `b`'s block `rank`: the all-to-all block transpose that swaps the g
 // global qubits with the top g local qubits.  peer >= 0: instead swap the
 // whole local state with that one rank (used by the deferred global flip).
+// Host barrier of an in-process group (600 s limit, like the reference's
+// receive timeout, sharded.py:38).
+int group_barrier(lrq_group* G) {
+  std::unique_lock<std::mutex> lk(G->mu);
+  if (G->broken) return fail(LRQ_ERUNTIME, "shard group aborted: " + G->why);
+  const unsigned long long my = G->gen;
+  if (++G->count == G->world) {
+    G->count = 0;
+    ++G->gen;
+    G->cv.notify_all();
+    return LRQ_OK;
+  }
+  if (!G->cv.wait_for(lk, std::chrono::seconds(600), [&] { return G->gen != my || G->broken; })) {
+    G->broken = true;
+    G->why = "barrier timeout";
+    G->cv.notify_all();
+  }
+  if (G->gen == my) return fail(LRQ_ERUNTIME, "shard group aborted: " + G->why);
+  return LRQ_OK;
+}
+
+void group_abort(lrq_group* G, const std::string& why) {
+  std::lock_guard<std::mutex> lk(G->mu);
+  if (!G->broken) G->why = why;
+  G->broken = true;
+  G->cv.notify_all();
+}
+
+// a[i] <-> b[i] over `bytes` (16-byte units; the blocks are 16-byte multiples)
+__global__ void swap_kernel(uint4* __restrict__ a, uint4* __restrict__ b, long long units) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < units;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint4 x = a[i], y = b[i];
+    a[i] = y;
+    b[i] = x;
+  }
+}
+
+int enable_peer(int dev, int peer) {
+  if (dev == peer) return LRQ_OK;
+  int ok = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&ok, dev, peer));
+  if (!ok) return fail(LRQ_ERUNTIME, "shard group spans devices without peer access");
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);  // on the current device (dev)
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return LRQ_OK;
+  }
+  CUDA_TRY(e);
+  return LRQ_OK;
+}
+
+// exchange_blocks for an in-process group: every rank's work so far is
+// complete (stream sync + barrier); the lower rank of each pair swaps the two
+// blocks in place; a second barrier publishes the result.
+int exchange_group(lrq_state* s, int peer) {
+  lrq_group* G = s->group;
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  int rc = group_barrier(G);
+  if (rc) return rc;
+  const size_t block = peer >= 0 ? (size_t)s->pbytes << s->n : (size_t)s->pbytes << (s->n - s->g);
+  const int grid = 4 * sm_count(s->device);
+  for (int b = s->rank + 1; b < s->world; ++b) {
+    if (peer >= 0 && b != peer) continue;
+    lrq_state* o = G->members[b];
+    rc = enable_peer(s->device, o->device);
+    if (rc) return rc;
+    unsigned char* mine = reinterpret_cast<unsigned char*>(s->amps) + (peer >= 0 ? 0 : (size_t)b * block);
+    unsigned char* theirs = reinterpret_cast<unsigned char*>(o->amps) + (peer >= 0 ? 0 : (size_t)s->rank * block);
+    swap_kernel<<<grid, 256, 0, s->stream>>>(reinterpret_cast<uint4*>(mine), reinterpret_cast<uint4*>(theirs),
+                                             (long long)(block / 16));
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return group_barrier(G);
+}
+
+// the sampler's sum over ranks for an in-process group (host buffers)
+int group_sum_shots(lrq_state* s, uint64_t* idx, int64_t shots) {
+  lrq_group* G = s->group;
+  {
+    std::lock_guard<std::mutex> lk(G->mu);
+    G->shot_bufs[s->rank] = idx;
+  }
+  int rc = group_barrier(G);
+  if (rc) return rc;
+  std::vector<uint64_t> sum((size_t)shots, 0);
+  for (int r = 0; r < G->world; ++r)
+    for (int64_t k = 0; k < shots; ++k) sum[k] += G->shot_bufs[r][k];
+  rc = group_barrier(G);
+  if (rc) return rc;
+  memcpy(idx, sum.data(), sizeof(uint64_t) * shots);
+  return LRQ_OK;
+}
+
 int exchange_blocks(lrq_state* s, int peer) {
+  if (s->group) return exchange_group(s, peer);
   NcclApi& nc = nccl();
   const size_t block = peer >= 0 ? (size_t)s->pbytes << s->n : (size_t)s->pbytes << (s->n - s->g);
   unsigned char* base = reinterpret_cast<unsigned char*>(s->amps);
@@ -562,6 +690,23 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
 
 // all ranks: the per-rank finalize scalars, gathered in rank order
 int gather_out(lrq_state* s, std::vector<double>& h) {
+  if (s->group) {
+    lrq_group* G = s->group;
+    double mine[4];
+    CUDA_TRY(cudaMemcpyAsync(mine, s->out, sizeof mine, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    {
+      std::lock_guard<std::mutex> lk(G->mu);
+      memcpy(&G->gather[4 * s->rank], mine, sizeof mine);
+    }
+    int rc = group_barrier(G);
+    if (rc) return rc;
+    {
+      std::lock_guard<std::mutex> lk(G->mu);
+      h = G->gather;
+    }
+    return group_barrier(G);  // nobody overwrites a slot before all have read
+  }
   NCCL_TRY(nccl().AllGather(s->out, s->dgather, 4, ncclDouble, s->comm, s->stream));
   h.resize(4 * s->world);
   CUDA_TRY(cudaMemcpyAsync(h.data(), s->dgather, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s->stream));
@@ -698,10 +843,11 @@ int lrq_destroy(lrq_state* s) {
   return LRQ_OK;
 }
 
-int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, const void* nccl_id,
-                    uint64_t memory_budget, lrq_state** out) {
-  if (!out || !nccl_id) return fail(LRQ_EVALIDATION, "null argument");
-  *out = nullptr;
+namespace {
+// common part of lrq_create_dist / lrq_create_shard: a rank's shard of
+// 2^(n_total-g) amplitudes plus the remap / gather buffers
+int create_rank_state(int n_total, int pbytes, int device, int rank, int world, uint64_t memory_budget,
+                      bool staging, lrq_state** out) {
   if (world < 2 || (world & (world - 1))) return fail(LRQ_EVALIDATION, "world size must be a power of two >= 2");
   if (rank < 0 || rank >= world) return fail(LRQ_EVALIDATION, "rank out of range");
   if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
@@ -711,8 +857,6 @@ int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, co
   if (nl <= KA) return fail(LRQ_EVALIDATION, "distributed engine needs n - log2(world) > " + std::to_string(KA));
   if (plan_groups(nl, pair_of(pbytes)).back().ntargets < g)
     return fail(LRQ_EVALIDATION, "last qubit group smaller than log2(world); choose another n");
-  NcclApi& nc = nccl();
-  if (!nc.ok) return fail(LRQ_ERUNTIME, nc.err);
   lrq_state* s = nullptr;
   int rc = lrq_create(nl, pbytes, device, memory_budget, &s);
   if (rc) return rc;
@@ -723,7 +867,7 @@ int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, co
   DeviceGuard guard(device);
   const size_t block = (size_t)pbytes << (nl - g);
   s->chunk = block < (64ull << 20) ? block : (64ull << 20);
-  cudaError_t e = cudaMalloc(&s->stage, s->chunk * (size_t)(world - 1));
+  cudaError_t e = staging ? cudaMalloc(&s->stage, s->chunk * (size_t)(world - 1)) : cudaSuccess;
   if (e == cudaSuccess) e = cudaMalloc(&s->dWx, sizeof(double) * nl);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->dWx, 0, sizeof(double) * nl, s->stream);
   if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * 4 * world);
@@ -732,6 +876,21 @@ int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, co
     free_state(s);
     return fail(LRQ_ECAPACITY, std::string("distributed buffers: ") + cudaGetErrorString(e));
   }
+  *out = s;
+  return LRQ_OK;
+}
+}  // namespace
+
+int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, const void* nccl_id,
+                    uint64_t memory_budget, lrq_state** out) {
+  if (!out || !nccl_id) return fail(LRQ_EVALIDATION, "null argument");
+  *out = nullptr;
+  NcclApi& nc = nccl();
+  if (!nc.ok) return fail(LRQ_ERUNTIME, nc.err);
+  lrq_state* s = nullptr;
+  int rc = create_rank_state(n_total, pbytes, device, rank, world, memory_budget, true, &s);
+  if (rc) return rc;
+  DeviceGuard guard(device);
   ncclUniqueId id;
   memcpy(&id, nccl_id, sizeof id);
   ncclResult_t r = nc.CommInitRank(&s->comm, world, id, rank);
@@ -740,6 +899,59 @@ int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, co
     free_state(s);
     return fail(LRQ_ERUNTIME, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
   }
+  *out = s;
+  return LRQ_OK;
+}
+
+int lrq_group_create(int world, lrq_group** out) {
+  if (!out) return fail(LRQ_EVALIDATION, "null argument");
+  *out = nullptr;
+  if (world < 2 || (world & (world - 1))) return fail(LRQ_EVALIDATION, "world size must be a power of two >= 2");
+  lrq_group* G = new lrq_group;
+  G->world = world;
+  G->members.assign(world, nullptr);
+  G->gather.assign(4 * (size_t)world, 0.0);
+  G->shot_bufs.assign(world, nullptr);
+  *out = G;
+  return LRQ_OK;
+}
+
+int lrq_group_abort(lrq_group* G) {
+  if (!G) return fail(LRQ_EVALIDATION, "null group");
+  group_abort(G, "aborted by the host");
+  return LRQ_OK;
+}
+
+int lrq_group_destroy(lrq_group* G) {
+  if (!G) return LRQ_OK;
+  {
+    std::lock_guard<std::mutex> lk(G->mu);
+    for (lrq_state* m : G->members)
+      if (m) return fail(LRQ_ERUNTIME, "destroy the group's shard states first");
+  }
+  delete G;
+  return LRQ_OK;
+}
+
+int lrq_create_shard(int n_total, int pbytes, int device, int rank, lrq_group* G, uint64_t memory_budget,
+                     lrq_state** out) {
+  if (!out || !G) return fail(LRQ_EVALIDATION, "null argument");
+  *out = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(G->mu);
+    if (rank < 0 || rank >= G->world) return fail(LRQ_EVALIDATION, "rank out of range");
+    if (G->members[rank]) return fail(LRQ_EVALIDATION, "rank already has a shard in this group");
+  }
+  lrq_state* s = nullptr;
+  int rc = create_rank_state(n_total, pbytes, device, rank, G->world, memory_budget, false, &s);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(G->mu);
+  if (G->members[rank]) {
+    free_state(s);
+    return fail(LRQ_EVALIDATION, "rank already has a shard in this group");
+  }
+  s->group = G;
+  G->members[rank] = s;
   *out = s;
   return LRQ_OK;
 }
@@ -789,7 +1001,11 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   for (int k = 0; k < p; ++k)
     if (!isfinite(mixer[k])) return fail(LRQ_EVALIDATION, "mixer angle is not finite");
   DeviceGuard guard(s->device);
-  if (s->world > 1) return run_dist(s, p, phase, mixer);
+  if (s->world > 1) {
+    const int rc = run_dist(s, p, phase, mixer);
+    if (rc && s->group) group_abort(s->group, g_err);
+    return rc;
+  }
   if (p > s->jcap) {
     cudaFree(s->dJ);
     cudaFree(s->dmix);
@@ -807,6 +1023,30 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   }
   CUDA_TRY(cudaMemcpyAsync(s->dJ, J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice, s->stream));
   CUDA_TRY(cudaMemcpyAsync(s->dmix, mix.data(), sizeof(double) * mix.size(), cudaMemcpyHostToDevice, s->stream));
+  const bool fields = !s->field_h.empty();
+  if (fields) {
+    if (p > s->fcap) {
+      cudaFree(s->dF);
+      s->dF = nullptr;
+      CUDA_TRY(cudaMalloc(&s->dF, sizeof(double) * (size_t)p * (n + 1)));
+      s->fcap = p;
+    }
+    // The sweep path defers the X^(x)n of flipped mixers (mixer_form): after
+    // an odd number of them the stored state is the index-reversed one, on
+    // which Z_i reads -Z_i.  Z-Z terms are invariant; single-Z fields flip.
+    std::vector<double> F(s->field_h);
+    F.insert(F.end(), s->cst_h.begin(), s->cst_h.end());
+    if (n >= s->K) {
+      int fl = 0;
+      for (int k = 0; k < p; ++k) {
+        if (fl & 1)
+          for (int i = 0; i < n; ++i) F[(size_t)k * n + i] = -F[(size_t)k * n + i];
+        fl += mixer_form(mixer[k]).flip;
+      }
+    }
+    CUDA_TRY(cudaMemcpyAsync(s->dF, F.data(), sizeof(double) * F.size(), cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));  // F is a local
+  }
 
   const double init = s->pbytes == 8 ? init_amplitude<float>(n) : init_amplitude<double>(n);
   s->reduced = false;
@@ -827,7 +1067,9 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.p = p;
     sp.J = s->dJ;
     sp.mix = s->dmix;
-    sp.W = s->have_cost ? s->dW : nullptr;
+    sp.W = s->dW;  // zero until a cost is set: sum p is still reduced
+    sp.F = fields ? s->dF : nullptr;
+    sp.Fc = fields ? s->dF + (size_t)p * n : nullptr;
     sp.init_re = init;
     sp.init_im = 0.0;
     sp.load = 0;
@@ -868,8 +1110,8 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.init_re = init;
       sp.init_im = 0.0;
       sp.J.M = w.phase >= 0 ? s->dJ + (size_t)w.phase * n * n : s->dW;
-      sp.J.ext = s->dzero;
-      sp.J.cst = 0.0;
+      sp.J.ext = fields && w.phase >= 0 ? s->dF + (size_t)w.phase * n : s->dzero;
+      sp.J.cst = fields && w.phase >= 0 ? s->cst_h[w.phase] : 0.0;
       sp.W.M = s->dW;
       sp.W.ext = s->dzero;
       sp.W.cst = 0.0;
@@ -915,6 +1157,25 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   return LRQ_OK;
 }
 
+int lrq_run_fields(lrq_state* s, int p, const double* phase, const double* field, const double* constant,
+                   const double* mixer) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (s->world > 1) return fail(LRQ_EVALIDATION, "lrq_run_fields is single-GPU only");
+  if (p < 1) return fail(LRQ_EVALIDATION, "depth p must be >= 1");
+  if (!field || !constant) return fail(LRQ_EVALIDATION, "null field/constant arrays");
+  const int n = s->n;
+  for (long long i = 0; i < (long long)p * n; ++i)
+    if (!isfinite(field[i])) return fail(LRQ_EVALIDATION, "field angle is not finite");
+  for (int k = 0; k < p; ++k)
+    if (!isfinite(constant[k])) return fail(LRQ_EVALIDATION, "constant phase is not finite");
+  s->field_h.assign(field, field + (size_t)p * n);
+  s->cst_h.assign(constant, constant + p);
+  const int rc = lrq_run(s, p, phase, mixer);
+  s->field_h.clear();
+  s->cst_h.clear();
+  return rc;
+}
+
 int lrq_recompute(lrq_state* s) {
   if (!s) return fail(LRQ_EVALIDATION, "null state");
   if (!s->ran) return fail(LRQ_ERUNTIME, "state holds no circuit result yet");
@@ -953,8 +1214,11 @@ int lrq_recompute(lrq_state* s) {
     sp.J.M = s->dW;
     sp.J.ext = s->dzero;
     sp.W.M = s->dW;
-    sp.W.ext = s->dzero;
-    sp.min_bit = n - 1;
+    // a shard: the rank's field / constant, and the max-cut search over
+    // global top bit 0 (the state is in the identity permutation after a run)
+    sp.W.ext = s->world > 1 ? s->dWx : s->dzero;
+    sp.W.cst = s->world > 1 ? s->wcst : 0.0;
+    sp.min_bit = s->world > 1 ? (((s->rank >> (s->g - 1)) & 1) ? -2 : -1) : n - 1;
     sp.red_p = rp;
     sp.red_pE = rpe;
     sp.red_minE = rmin;
@@ -967,6 +1231,7 @@ int lrq_recompute(lrq_state* s) {
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->reduced = true;
+  s->rank_sum_p.clear();
   return LRQ_OK;
 }
 
@@ -980,7 +1245,10 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
     // local argmin -> global index (rank bits on top, identity permutation)
     std::vector<double> all;
     int rc = gather_out(s, all);
-    if (rc) return rc;
+    if (rc) {
+      if (s->group) group_abort(s->group, g_err);
+      return rc;
+    }
     double sp = 0.0, spe = 0.0, mn = __builtin_inf();
     uint64_t best = ~0ull;
     s->rank_sum_p.assign(s->world, 0.0);
@@ -1060,10 +1328,15 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
     sample_kernel<double><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
                                                                     shots, off, total, base_index, s->didx);
   CUDA_TRY(cudaGetLastError());
-  if (s->world > 1)  // exactly one rank owns each shot; the others wrote 0
+  if (s->world > 1 && !s->group)  // exactly one rank owns each shot; the others wrote 0
     NCCL_TRY(nccl().AllReduce(s->didx, s->didx, shots, ncclUint64, ncclSum, s->comm, s->stream));
   CUDA_TRY(cudaMemcpyAsync(idx, s->didx, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->group) {
+    const int rc = group_sum_shots(s, idx, shots);
+    if (rc) group_abort(s->group, g_err);
+    return rc;
+  }
   return LRQ_OK;
 }
 

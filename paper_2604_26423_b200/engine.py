@@ -124,6 +124,14 @@ class StateVector:
                 self._dev.recompute()
         return self._dev.reduce()
 
+    def _copy_range(self, start: int, count: int) -> np.ndarray:
+        return self._dev.copy_amps(start, count)
+
+    def _draw(self, u: np.ndarray) -> np.ndarray:
+        """Global indices of the inverse-CDF draws for uniforms u."""
+        self._reductions(None)
+        return self._dev.sample(u)
+
     def norm_squared(self) -> float:
         return float(self._reductions(None).sum_p)
 
@@ -191,9 +199,7 @@ def sample(sv: StateVector, n_shots: int, rng_seed: int) -> ShotSet:
     if n_shots < 1:
         raise ValidationError(f"shot count must be positive, got {n_shots}")
     u = derive_rng(rng_seed, "shots", 0).random(n_shots)
-    sv._reductions(None)
-    idx = sv.device_state.sample(u)
-    return ShotSet(sv.num_qubits, idx, int(rng_seed), "noiseless")
+    return ShotSet(sv.num_qubits, sv._draw(u), int(rng_seed), "noiseless")
 
 
 # ---------------------------------------------------------------------------
@@ -211,7 +217,7 @@ def save_statevector(sv: StateVector, path: str | Path) -> None:
         chunk = 1 << 24
         total = 1 << sv.num_qubits
         for lo in range(0, total, chunk):
-            part = sv.device_state.copy_amps(lo, min(chunk, total - lo))
+            part = sv._copy_range(lo, min(chunk, total - lo))
             fh.write(np.ascontiguousarray(part, dtype=code).tobytes())
 
 
