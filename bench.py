@@ -19,8 +19,12 @@ roofline  dominant kernel = sweep_kernel; algorithmic bytes per launch =
         2 * 2^n * B (B = 8 for complex64; the first, write-only sweep 2^n*B),
         divided by its CUDA-event duration on the engine stream.
 
-Multi-GPU (--gpus N under torchrun): N independent replicas of the workload,
-one per rank (weak scaling); see DESIGN.md §5 for the global-qubit path.
+Multi-GPU (--gpus N under torchrun, one process per GPU): ONE state of
+n + log2(N) qubits distributed over the N GPUs (weak scaling: 2^n amplitudes
+per GPU), run by the distributed engine: local fused sweeps, one NCCL block
+transpose of the global qubits per layer, collective reductions and sampler
+(DESIGN.md §5).  torch.distributed (gloo) only bootstraps the NCCL id and the
+max-over-ranks timing.
 """
 from __future__ import annotations
 
@@ -336,10 +340,140 @@ def run_ours(args, rank, world, local_rank, dist):
     return out
 
 
+def run_ours_dist(args, rank, world, local_rank, dist):
+    """N > 1: one distributed state of n + log2(N) qubits (weak scaling)."""
+    os.environ.setdefault("LRQ_DEVICE", str(local_rank))
+    import paper_2604_26423_b200 as L
+    from paper_2604_26423_b200 import _native
+    from paper_2604_26423_b200.build import build
+    from paper_2604_26423_b200.distributed import drain_dist_pool, run_circuit_distributed
+
+    if rank == 0:
+        build()
+    barrier(dist)
+    import torch
+
+    dev_index = int(os.environ["LRQ_DEVICE"])
+    torch.cuda.set_device(dev_index)
+    g = world.bit_length() - 1
+    if (1 << g) != world:
+        raise SystemExit("--gpus must be a power of two")
+    n, p = args.n + g, args.p
+    nl = args.n
+    B = 8 if args.precision == "fp32" else 16
+    inst = L.generate_instance(n, args.seed)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=p))
+    lay = L.lower_circuit(circ)
+    w = inst.weights()
+    u = L.derive_rng(1, "shots", 0).random(args.shots)
+
+    box = [_native.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    dev = _native.DeviceState.create_dist(n, B, dev_index, rank, world, box[0])
+    dev.set_cost(w)
+    stream = torch.cuda.ExternalStream(dev.stream())
+    for _ in range(args.warmup):
+        dev.run(lay.phase, lay.mixer)
+        dev.sample(u)
+    dev.set_timing(True)
+    ms_all, kinds_all = [], ""
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev_index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            dev.run(lay.phase, lay.mixer)
+            ms, kinds = dev.timings()
+            ms_all += ms
+            kinds_all += kinds
+            dev.sample(u)
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    barrier(dist)
+    dev_ms_max = max_over_ranks(dist, e0.elapsed_time(e1))
+    red = dev.reduce()
+    dev.close()
+
+    z = int(red.argmax_cut)
+    solved = L.WmcInstance(inst.num_vertices, inst.edges, inst.seed,
+                           L.OptimalCut(L.index_to_bitstring(z, n), float(L.cut_values(inst, [z])[0])))
+    sv = run_circuit_distributed(circ, args.precision)  # warm: NCCL communicator, pooled shard
+    sv.exact_expected_r(solved)
+    sv.sample(args.shots, 1)
+    sv.release()
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sv = run_circuit_distributed(circ, args.precision)
+        r_exact = sv.exact_expected_r(solved)
+        shots = sv.sample(args.shots, 1)
+        sv.release()
+    e2e_s_max = max_over_ranks(dist, time.perf_counter() - t0)
+    r_sampled = L.approximation_ratio(solved, shots)
+    drain_dist_pool()
+    _native.drain_pool()
+    if rank != 0:
+        return None
+
+    sw = [(m, k) for m, k in zip(ms_all, kinds_all) if k in "PMFRQ"]
+    alg = sum((1 if k in "PQ" else 2) * (B << nl) for _, k in sw)
+    sweep_time_s = sum(m for m, _ in sw) * 1e-3
+    achieved = alg / sweep_time_s / 1e9
+    remap_ms = [m for m, k in zip(ms_all, kinds_all) if k == "T"]
+    remap_bytes = (world - 1) * (B << (nl - g))  # sent (= received) per GPU per remap
+    peak, peak_kind = measured_peak()
+    amp_updates = float(1 << n) * p * args.steps
+    E = n * (n - 1) // 2
+    launches_per_step = len(ms_all) // args.steps + 1
+    return {
+        "metric": METRIC,
+        "value": amp_updates / (dev_ms_max * 1e-3),
+        "unit": "amp-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dev_ms_max / args.steps,
+        "ms_per_layer": dev_ms_max / args.steps / p,
+        "gate_equiv_amp_updates_per_s": amp_updates * (E + n) / (dev_ms_max * 1e-3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 amplitudes, fp64 phases and reductions)" if B == 8 else "c128 (fp64)",
+        "data": "synthetic: generate_instance(n, seed) Philox weights, LrQaoaParams(p) default ramp",
+        "config": {"workload": f"LR-QAOA p={p}, n={n} fully connected weighted MaxCut, "
+                               f"{'complex64' if B == 8 else 'complex128'}, one state over {world} B200s "
+                               f"(2^{nl} amplitudes per GPU)",
+                   "n": n, "n_local": nl, "p": p, "precision": args.precision, "shots": args.shots,
+                   "state_bytes": B << n, "parallelism": f"global-qubit sharding x{world} (NCCL remap per layer)",
+                   "l2": "shard >> L2 (126 MB); no flush needed"},
+        "e2e": {"value": amp_updates / e2e_s_max, "unit": "amp-updates/s",
+                "h2d_bytes_per_step": int(lay.phase.nbytes + lay.mixer.nbytes + w.nbytes + args.shots * 8),
+                "d2h_bytes_per_step": int(args.shots * 8 + 32 * world),
+                "api": "run_circuit_distributed -> exact_expected_r -> sample (collective, ctypes C-ABI)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_kind, "traffic": None, "kernel": "sweep_kernel (local shard)",
+                     "bytes_per_launch": 2 * (B << nl), "launch_ms_avg": sweep_time_s * 1e3 / max(1, len(sw))},
+        "remap": {"per_step": len(remap_ms) // args.steps, "ms_avg": statistics.mean(remap_ms) if remap_ms else None,
+                  "bytes_sent_per_gpu": remap_bytes,
+                  "algbw_GBps": remap_bytes / (statistics.mean(remap_ms) * 1e-3) / 1e9 if remap_ms else None},
+        "sweep_ms": {k: round(statistics.mean(m for m, kk in sw if kk == k), 3) for k in sorted(set(kinds_all))
+                     if k in "PMFRQ"},
+        "gpu_launches": launches_per_step * args.steps,
+        "cpu_baseline": None,
+        "clocks": clk.summary(),
+        "results": {"exact_r": r_exact, "sampled_r": r_sampled, "sum_p": red.sum_p,
+                    "max_cut": solved.optimal_cut.value},
+    }
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    cpu = cpu_reference(args.n, args.p, args.precision, args.cpu_seconds, args.seed)
+    # same workload as our arm: one state of n + log2(N) qubits
+    n = args.n + (world.bit_length() - 1)
+    cpu = cpu_reference(n, args.p, args.precision, args.cpu_seconds, args.seed)
     t_step = cpu["t_layer_s"] * args.p
     return {
         "impl": "reference",
@@ -355,8 +489,8 @@ def run_reference(args, rank, world):
         "vs_baseline": None,
         "dtype": "c64" if args.precision == "fp32" else "c128",
         "data": "synthetic",
-        "config": {"workload": f"LR-QAOA p={args.p}, n={args.n}, reference per-gate CPU engine (oracle port)",
-                   "n": args.n, "p": args.p, "precision": args.precision},
+        "config": {"workload": f"LR-QAOA p={args.p}, n={n}, reference per-gate CPU engine (oracle port)",
+                   "n": n, "p": args.p, "precision": args.precision},
         "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cpu["value"], "unit": "amp-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -369,7 +503,7 @@ def main():
         out = run_reference(args, rank, world)
     else:
         dist = init_dist(world)
-        out = run_ours(args, rank, world, local_rank, dist)
+        out = (run_ours_dist if world > 1 else run_ours)(args, rank, world, local_rank, dist)
         if dist is not None:
             dist.destroy_process_group()
     if out is not None:

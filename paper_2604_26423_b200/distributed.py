@@ -60,23 +60,34 @@ class DistStateVector:
     def norm_squared(self) -> float:
         return float(self.reduce().sum_p)
 
+    def _reductions(self, weights: np.ndarray | None):
+        """Collective: final-pass reductions for cost `weights` (None: the
+        cost the run was fused with).  Another cost re-runs the read-only
+        pass on every rank."""
+        if weights is not None and (self._cost is None or not np.array_equal(self._cost, weights)):
+            self._dev.set_cost(weights)
+            self._dev.recompute()
+            self._cost = np.array(weights, dtype=np.float64)
+        return self._dev.reduce()
+
+    def _draw(self, u: np.ndarray) -> np.ndarray:
+        return self._dev.sample(u)
+
     def exact_expected_r(self, inst: WmcInstance) -> float:
+        """Collective; same as engine.exact_expected_r(self, inst)."""
         if inst.num_vertices != self.num_qubits:
             raise ValidationError(
                 f"instance has {inst.num_vertices} vertices, state has {self.num_qubits} qubits")
         if inst.optimal_cut is None:
             raise StateError("instance has no optimal cut; solve it first")
-        w = inst.weights()
-        if self._cost is None or not np.array_equal(self._cost, w):
-            raise ValidationError("the distributed final pass was fused with another cost; "
-                                  "build the circuit from this instance")
-        return float(self.reduce().sum_p_cut) / inst.optimal_cut.value
+        return float(self._reductions(inst.weights()).sum_p_cut) / inst.optimal_cut.value
 
     def sample(self, n_shots: int, rng_seed: int) -> ShotSet:
+        """Collective; the same global indices on every rank."""
         if n_shots < 1:
             raise ValidationError(f"shot count must be positive, got {n_shots}")
         u = derive_rng(rng_seed, "shots", 0).random(n_shots)
-        return ShotSet(self.num_qubits, self._dev.sample(u), int(rng_seed), "noiseless")
+        return ShotSet(self.num_qubits, self._draw(u), int(rng_seed), "noiseless")
 
     def local_amps(self) -> np.ndarray:
         return self._dev.copy_amps()
@@ -96,7 +107,28 @@ class DistStateVector:
         return np.concatenate([p.numpy().view(dt) for p in parts])
 
     def release(self) -> None:
-        self._dev.close()
+        """Park the shard for the next run_circuit_distributed of the same
+        shape (all ranks release in step, so the pools stay symmetric)."""
+        if self._dev is None:
+            return
+        key = (self.num_qubits, self._precision.bytes_per_amplitude, self._dev.device, self.rank, self.world,
+               id(self._group))
+        if key not in _DIST_POOL:
+            _DIST_POOL[key] = self._dev
+        else:
+            self._dev.close()
+        self._dev = None
+
+
+# Parked shards: NCCL communicator setup costs far more than a small run, so
+# a loop of run_circuit_distributed reuses one shard (and its communicator).
+_DIST_POOL: dict = {}
+
+
+def drain_dist_pool() -> None:
+    while _DIST_POOL:
+        _, dev = _DIST_POOL.popitem()
+        dev.close()
 
 
 def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Precision.FP32, group=None,
@@ -112,11 +144,13 @@ def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Pre
     g = world.bit_length() - 1
     check_memory(n - g, precision, memory_budget)
     layers = lower_circuit(circuit)
-    box = [_native.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0, group=group)
     dev_index = _native.default_device() if device is None else int(device)
-    dev = _native.DeviceState.create_dist(n, precision.bytes_per_amplitude, dev_index, rank, world, box[0],
-                                          int(memory_budget or 0))
+    dev = _DIST_POOL.pop((n, precision.bytes_per_amplitude, dev_index, rank, world, id(group)), None)
+    if dev is None:
+        box = [_native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        dev = _native.DeviceState.create_dist(n, precision.bytes_per_amplitude, dev_index, rank, world, box[0],
+                                              int(memory_budget or 0))
     cost = getattr(circuit, "cost_weights", None)
     dev.set_cost(cost if cost is not None else np.zeros(n * (n - 1) // 2))
     dev.run(layers.phase, layers.mixer)
