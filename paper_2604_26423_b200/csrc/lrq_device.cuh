@@ -91,12 +91,25 @@ __device__ __forceinline__ float2 phasor32(double angle) {
   sincosf(r, &s, &co);
   return make_float2(co, -s);
 }
+#ifdef LRQ_EXPLICIT_FFMA2
+// packed complex products: one FMUL2 + one FFMA2 (the broadcasts, lane swaps
+// and one-lane negations are operand modifiers in SASS)
+// a b = a.x b + a.y (i b),  i b = (-b.y, b.x)
+__device__ __forceinline__ float2 cmul32(float2 a, float2 b) {
+  return ffma2(make_float2(a.y, a.y), make_float2(-b.y, b.x), fmul2(make_float2(a.x, a.x), b));
+}
+// a conj(b) = b.x a + b.y (-i a),  -i a = (a.y, -a.x)
+__device__ __forceinline__ float2 cmul32_conj(float2 a, float2 b) {
+  return ffma2(make_float2(b.y, b.y), make_float2(a.y, -a.x), fmul2(make_float2(b.x, b.x), a));
+}
+#else
 __device__ __forceinline__ float2 cmul32(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 cmul32_conj(float2 a, float2 b) {  // a * conj(b)
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
+#endif
 __device__ __forceinline__ float2 conj32(float2 a) { return make_float2(a.x, -a.y); }
 
 // ---------------------------------------------------------------------------
@@ -107,6 +120,10 @@ __device__ __forceinline__ float2 conj32(float2 a) { return make_float2(a.x, -a.
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 // named barrier `id` over one 256-thread team
 __device__ __forceinline__ void team_sync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+// named barrier `id` over `count` threads (a multiple of 32)
+__device__ __forceinline__ void team_sync_n(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // ---- mbarrier / TMA primitives ---------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }

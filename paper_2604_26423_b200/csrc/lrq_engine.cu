@@ -18,6 +18,7 @@
 #include "lrq_plan.h"
 #include "lrq_dist.cuh"
 #include "lrq_sweep_tma.cuh"
+#include "lrq_sweep_wd.cuh"
 
 using namespace lrq;
 
@@ -383,6 +384,38 @@ bool use_tma_path(int pbytes, int gk, int sk) {
   return pbytes == 8 && gk != GK_A && (sk == SK_M || sk == SK_F);
 }
 
+template <int GK, int SK>
+int launch_wd_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(sweep_wd_kernel<GK, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  CUDA_TRY(err);
+  sweep_wd_kernel<GK, SK><<<grid, kWdThreads, smem, st>>>(sp);
+  CUDA_TRY(cudaGetLastError());
+  return LRQ_OK;
+}
+
+// warp-decoupled complex64 high-group sweep (plan prog 1): TMA ring of 3
+// stages, 2 tiles in flight, one CTA per SM
+int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
+  SweepParams sp = sp_in;
+  const int K = tile_amp_bits(s->pbytes);
+  const int ma = group_ma(gk, 1);
+  if (!make_tile_tmap(&sp.tmap, s->amps, gk, sp.n, s->pbytes, ma, K, sp.q0, s->num_tiles))
+    return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
+  sp.has_tmap = 1;
+  sp.nstages = 3;
+  const size_t smem = wd_smem_bytes(sp.n, 3, sk == SK_F);
+  if (smem > 227 * 1024) return fail(LRQ_ERUNTIME, "internal: warp-decoupled sweep needs too much shared memory");
+  const int sms = sm_count(s->device);
+  const int g = (int)(s->num_tiles < sms ? s->num_tiles : sms);
+  if (gk == GK_H) return sk == SK_F ? launch_wd_t<GK_H, SK_F>(s->stream, sp, g, smem)
+                                    : launch_wd_t<GK_H, SK_M>(s->stream, sp, g, smem);
+  return sk == SK_F ? launch_wd_t<GK_H4, SK_F>(s->stream, sp, g, smem) : launch_wd_t<GK_H4, SK_M>(s->stream, sp, g, smem);
+}
+
 int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int grid) {
   const bool amps = sk != SK_N;
   const bool usesJ = sk == SK_P || sk == SK_F || sk == SK_L;
@@ -396,7 +429,9 @@ int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int gri
       return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
     sp.has_tmap = 1;
     const size_t cap = 227 * 1024;
-    int teams = env_int("LRQ_TMA_TEAMS", 1);  // 2 teams measured no faster (profiles/r01_*)
+    // F sweeps (two mixers + phase) overlap better with two independent teams;
+    // the lighter M sweeps stream best with one team and 255 registers
+    int teams = env_int("LRQ_TMA_TEAMS", sk == SK_F ? 2 : 1);
     teams = teams == 1 ? 1 : 2;
     if (teams == 2 && tma_smem_bytes(sp.n, 3, 2, usesJ, usesW) > cap) teams = 1;
     sp.nstages = tma_smem_bytes(sp.n, 3, teams, usesJ, usesW) <= cap ? 3 : 2;
@@ -1120,7 +1155,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.red_pE = rpe;
       sp.red_minE = rmin;
       sp.red_arg = rarg;
-      int rc = launch_sweep(s, g.kind, w.kind, sp, grid);
+      int rc = w.prog == 1 ? launch_wd(s, g.kind, w.kind, sp) : launch_sweep(s, g.kind, w.kind, sp, grid);
       if (rc) return rc;
       record(s, ev++, "PMFRLQN"[w.kind]);
     }

@@ -16,7 +16,9 @@
 //            assigns which register bits take a butterfly in which round.
 #pragma once
 #include <stdint.h>
+#include <stdlib.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -45,6 +47,8 @@ struct PlanSweep {
   int ntarget1, ntarget2;  // qubits mixed by mixer 1 / 2 (scale factor powers)
   bool remap_after;        // distributed plans: a qubit remap follows this sweep
   int perm;                // permutation state the sweep runs in (0 identity, 1 swapped)
+  int prog;                // 0: round programs of sweep_kernel / sweep_tma_kernel;
+                           // 1: warp-decoupled 2-layout program (lrq_sweep_wd.cuh)
 };
 
 struct Plan {
@@ -76,7 +80,9 @@ inline std::vector<PlanGroup> plan_groups(int n, int pair) {
     n_h4 = nh - (need10 > 0 ? need10 : 0);
   }
   for (int i = 0, g0 = KA; g0 < n; ++i) {
-    const int kind = i < n_h4 ? GK_H4 : GK_H;
+    // H4 groups last: the last group takes the fused F sweeps, and its 128 B
+    // runs stream better than the 64 B runs of an H group
+    const int kind = i >= nh - n_h4 ? GK_H4 : GK_H;
     const int MA = group_ma(kind, pair);
     const int kmax = KA - MA;
     const int k = (n - g0) < kmax ? (n - g0) : kmax;
@@ -100,7 +106,41 @@ inline std::vector<PlanGroup> plan_groups(int n, int pair) {
 // register bit that is not one of the group's targets gets tangent 0.
 // mask*[r] = register amp bits that take a real butterfly in round r,
 // tmask*[r] = the same bits as tile amp bits.
+// warp-decoupled program (complex64 H/H4, M and F sweeps): layout L1 holds
+// tile amp bits 8..12 in registers, L2 bits 3..7; rounds M: L1, L2;
+// F: L1 (mix1), L2 (mix1, phase, mix2), L1 (mix2).  Register amp bit a
+// (1..5) is tile amp bit (L1 ? 7 : 2) + a; bit 0 (the pair bit) is a run bit.
+// Its tangent goes to SweepParams::tf[w][r][a - 1].
+inline int wd_layout(int kind, int r) { return (kind == SK_F && r == 1) || (kind == SK_M && r == 1) ? 2 : 1; }
+inline void plan_rounds_wd(const PlanGroup& g, PlanSweep& sw) {
+  sw.nrounds = sw.kind == SK_F ? 3 : 2;
+  const unsigned targets[2] = {sw.target1 ? sw.target1 : g.tmask, g.tmask};
+  if (!sw.ntarget1) sw.ntarget1 = sw.target1 ? __builtin_popcount(sw.target1) : g.ntargets;
+  if (!sw.ntarget2) sw.ntarget2 = g.ntargets;
+  for (int r = 0; r < sw.nrounds; ++r) {
+    const int L = wd_layout(sw.kind, r);
+    const bool mixes[2] = {sw.kind == SK_M || r < 2, sw.kind == SK_F && r >= 1};
+    unsigned m[2] = {0, 0}, tm[2] = {0, 0};
+    for (int w = 0; w < 2; ++w)
+      for (int a = 1; a <= 5; ++a) {
+        const unsigned tb = 1u << ((L == 1 ? 7 : 2) + a);
+        if (mixes[w] && (targets[w] & tb)) {
+          m[w] |= 1u << (a - 1);  // tangent slot k = a - 1 (the pair bit never mixes)
+          tm[w] |= tb;
+        }
+      }
+    sw.mask1[r] = sw.beta1 >= 0 ? m[0] : 0;
+    sw.mask2[r] = sw.beta2 >= 0 ? m[1] : 0;
+    sw.tmask1[r] = sw.beta1 >= 0 ? tm[0] : 0;
+    sw.tmask2[r] = sw.beta2 >= 0 ? tm[1] : 0;
+  }
+}
+
 inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
+  if (sw.prog == 1) {
+    plan_rounds_wd(g, sw);
+    return;
+  }
   const int RA = 4 + pair;
   sw.nrounds = prog_rounds(g.kind, pair, sw.kind);
   const unsigned targets[2] = {sw.target1 ? sw.target1 : g.tmask, g.tmask};
@@ -138,6 +178,7 @@ inline PlanSweep make_sweep(int group, int kind, int b1, int ph, int b2, bool re
   s.ntarget1 = s.ntarget2 = 0;
   s.remap_after = false;
   s.perm = 0;
+  s.prog = 0;
   for (int r = 0; r < kMaxRounds; ++r) s.mask1[r] = s.mask2[r] = s.tmask1[r] = s.tmask2[r] = 0;
   return s;
 }
@@ -151,6 +192,54 @@ inline Plan make_plan(int n, int pair, int p) {
   if (P.small || p < 1) return P;
   P.groups = plan_groups(n, pair);
   const int S = (int)P.groups.size();
+  if (pair && S >= 3) {
+    // complex64 with >= 2 high groups: the fused F sweeps go to the two end
+    // HIGH groups (warp-decoupled kernel, two transposes), group A sits in
+    // the middle (M sweeps) and takes the final reduction: the last layer
+    // visits its remaining groups with A last.
+    //   order  E1=G_1, mids = A, G_2..G_{S-2}, E2 = G_{S-1}
+    std::vector<int> seq;
+    seq.push_back(1);
+    seq.push_back(0);
+    for (int i = 2; i < S - 1; ++i) seq.push_back(i);
+    seq.push_back(S - 1);
+    const char* nowd = getenv("LRQ_NO_WD");  // debugging: classic kernels, same order
+    auto wd = [&](int gi, int kind) {
+      // F only: a lone high-group M (last layer) streams faster on the classic TMA kernel
+      return !(nowd && *nowd == '1') && P.groups[gi].kind != GK_A && kind == SK_F ? 1 : 0;
+    };
+    auto push = [&](int gi, int kind, int b1, int ph, int b2, bool red) {
+      PlanSweep w = make_sweep(gi, kind, b1, ph, b2, red);
+      w.prog = wd(gi, kind);
+      P.sweeps.push_back(w);
+    };
+    // layer k (< p-1) visits seq forward for even k, backward for odd k; its
+    // last group is layer k+1's first (one F sweep); layer p-1 visits the
+    // groups it has left with A last (R)
+    auto layer_order = [&](int k) {
+      std::vector<int> o(seq);
+      if (k % 2) std::reverse(o.begin(), o.end());
+      return o;
+    };
+    for (int k = 0; k < p; ++k) {
+      std::vector<int> o = layer_order(k);
+      if (k == p - 1) {
+        // keep o[0] first (entered by the previous F, or P), put A last
+        std::vector<int> rest;
+        for (size_t i = 1; i < o.size(); ++i)
+          if (o[i] != 0) rest.push_back(o[i]);
+        rest.push_back(0);
+        o.resize(1);
+        o.insert(o.end(), rest.begin(), rest.end());
+      }
+      if (k == 0) push(o[0], SK_P, -1, 0, 0, false);
+      for (size_t i = 1; i + 1 < o.size(); ++i) push(o[i], SK_M, k, -1, -1, false);
+      if (k + 1 < p) push(o.back(), SK_F, k, k + 1, k + 1, false);
+      else push(o.back(), SK_R, k, -1, -1, true);
+    }
+    for (PlanSweep& w : P.sweeps) plan_rounds(P.groups[w.group], pair, w);
+    return P;
+  }
   if (S == 1) {
     P.sweeps.push_back(make_sweep(0, SK_P, -1, 0, 0, false));
     for (int k = 1; k < p; ++k) P.sweeps.push_back(make_sweep(0, SK_L, -1, k, k, k == p - 1));
@@ -246,11 +335,16 @@ inline std::string plan_json(const Plan& P) {
          ",\"reduce\":" + (w.reduce ? "true" : "false") + ",\"rounds\":[";
     for (int r = 0; r < w.nrounds; ++r) {
       s += (r ? "," : "");
+      if (w.prog == 1) {  // lo: the lowest register unit bit of the layout
+        s += "[" + std::to_string(wd_layout(w.kind, r) == 1 ? 7 : 2) + "," + std::to_string(w.tmask1[r]) + "," +
+             std::to_string(w.tmask2[r]) + "," + (w.kind == SK_F && r == 1 ? "1" : "0") + ",0]";
+        continue;
+      }
       s += "[" + std::to_string(prog_lo(g.kind, P.pair, w.kind, r)) + "," + std::to_string(w.tmask1[r]) + "," +
            std::to_string(w.tmask2[r]) + "," + (prog_phase(w.kind, g.kind, P.pair, r) ? "1" : "0") + "," +
            (prog_reduce(w.kind, g.kind, P.pair, r) ? "1" : "0") + "]";
     }
-    s += "]}";
+    s += "],\"prog\":" + std::to_string(w.prog) + "}";
   }
   s += "]}";
   return s;

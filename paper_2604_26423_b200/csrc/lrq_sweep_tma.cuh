@@ -157,8 +157,11 @@ __global__ void __launch_bounds__(TEAMS* kThreads, 1) sweep_tma_kernel(const __g
   const int nst = P.nstages;
   const bool usesW = HAS_REDUCE && (SK != SK_L || P.reduce);
 
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment for the swizzled TMA stages, as an offset into the
+  // __shared__ array: a pointer laundered through uintptr_t would lose the
+  // address space and turn every stage / table access into a generic LD/ST
+  const unsigned smem_off = (1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u;
+  unsigned char* smem = smem_raw + smem_off;
   unsigned char* stages = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * kStageBytes);
   unsigned char* sp = smem + (size_t)nst * kStageBytes + 64;

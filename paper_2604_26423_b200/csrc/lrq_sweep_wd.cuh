@@ -1,0 +1,347 @@
+// Warp-decoupled sweeps of a complex64 high qubit group (H: 64 B runs, H4:
+// 128 B runs), for the mixer-only (M) and the fused mix -> phase -> mix (F)
+// sweeps.  DESIGN.md §3.2.
+//
+// A high-group tile is 2^(KA-MA) runs of 2^MA contiguous amplitudes; the run
+// bits are NOT mixer targets in this sweep.  Unit bits 0-1 of the tile (inside
+// every run) therefore never need a butterfly, and they pick the warp: each
+// of the tile's 4 warps owns the 1024 units with its value of those bits and
+// exchanges no data with the other three.  Inside a warp the 10 remaining
+// unit bits are split 5 lanes x 5 registers (32 float4 units = 64 amplitudes
+// per thread), so two layouts cover every target:
+//     L1: lane = unit bits 2..6, registers = unit bits 7..11
+//     L2: lane = unit bits 7..11, registers = unit bits 2..6
+// M = L1 mix, L2 mix; F = L1 mix1, L2 mix1 + phase + mix2, L1 mix2.  Both
+// go L1 -> L2 -> L1 through a padded per-warp transpose region (two
+// transposes, __syncwarp only), because L1 is the layout whose reads and
+// writes of the TMA tile are bank-conflict free.
+//
+// Per tile: TMA tensor load into a stage (3-stage ring, one full mbarrier
+// per stage and team); L1 read; a 4-warp named barrier hands the stage over
+// as four 32 x 33-unit transpose regions; at the end a second 4-warp barrier
+// pair brackets the write-back in the TMA layout, one thread issues the TMA
+// tensor store, waits for it to have read the stage, and loads the tile nst
+// steps ahead into it.  Two tiles are in flight per CTA (8 warps, 2 per SM
+// sub-partition, which keeps 255 registers for the 64 amplitudes a thread
+// holds); the two teams run out of phase.
+//
+// Bank conflicts: the TMA swizzle puts unit e at e ^ ((e >> 3) & SWM); L1
+// accesses of the TMA layout have lanes on unit bits 2..4 -> 8 distinct
+// 16-byte bank groups per quarter warp; the transposes use slot().
+#pragma once
+#include "lrq_sweep_tma.cuh"
+
+namespace lrq {
+
+constexpr int kWdTeams = 2;  // tiles in flight per CTA
+constexpr int kWdWarps = 4;  // warps per tile
+constexpr int kWdThreads = kWdTeams * kWdWarps * 32;  // no producer warp (see refill)
+constexpr int kWdTT = kWdWarps * 32;  // tile threads
+constexpr int kWdRA = 6;              // register amp bits: pair + 5 unit bits
+// a stage holds the 64 KB TMA tile plus 2 KB so that, after the tile is read,
+// each warp owns a padded 32 x 33-unit transpose region of it
+constexpr int kWdStageBytes = 66 * 1024;
+constexpr int kWdRegion = 32 * 33;  // units per warp region
+
+__host__ __device__ inline size_t wd_smem_bytes(int n, int nst, bool usesJ) {
+  size_t b = (size_t)nst * kWdStageBytes + 128;  // stages + full barriers
+  if (usesJ) b = align16(b + 8 * (size_t)(n * n + n));
+  b += 8 * (size_t)((kWdRA + 1) * kWdTT);  // per-tile-thread constants
+  b += 8 * 64;                             // PRR32 (float2 x 64)
+  b += 8 * (size_t)(kWdTeams * 16);  // per-team hb[13] + ebb
+  b += 4 * 64;                         // block-bit list
+  return align16(b) + 1024;
+}
+
+template <int GK, int SK>
+struct WdSweep {
+  static_assert(GK == GK_H || GK == GK_H4, "warp-decoupled sweeps serve complex64 high groups");
+  static constexpr int MA = group_ma(GK, 1);  // run amp bits (3 or 4)
+  static constexpr int MU = MA - 1;           // run unit bits (2 or 3)
+  static constexpr int SWM = GK == GK_H ? 3 : 7;
+  static constexpr bool PH = SK == SK_F;
+
+  __device__ static __forceinline__ int swz(int e) { return e ^ ((e >> 3) & SWM); }
+  // unit (a, b) of warp wq: natural TMA position / transposed slot
+  __device__ static __forceinline__ int nat(int wq, int a, int b) { return swz(wq | (a << 2) | (b << 7)); }
+  // transposed unit (a, b) in the warp's region: row a, column b, rows padded
+  // to 33 units -> bank group (a + b) & 7, conflict-free for a lane-a writer
+  // and a lane-b reader, and base + immediate addressing both ways
+  __device__ static __forceinline__ int slot(int a, int b) { return a * 33 + b; }
+  // tile amp bit of register amp bit r (0 = pair) in layout L (1: regs = unit
+  // bits 7..11, 2: regs = unit bits 2..6)
+  __host__ __device__ static constexpr int reg_bit(int L, int r) { return r == 0 ? 0 : (L == 1 ? 7 : 2) + r; }
+  // tile amp bit of tile-thread bit j (warp bits 0-1, then the 5 lane bits)
+  __host__ __device__ static constexpr int thr_bit(int L, int j) { return j < 2 ? 1 + j : (L == 1 ? 3 : 8) + (j - 2); }
+
+  __device__ static __forceinline__ int gpos(int i, int q0) { return i < MA ? i : q0 + (i - MA); }
+
+  // butterflies on register unit bits of MASK (x + i t y, y + i t x) on both
+  // amplitudes of each unit
+  template <unsigned MASK>
+  __device__ static __forceinline__ void mix(float4 (&r)[32], const float* tf) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (!((MASK >> k) & 1u)) continue;
+      const float t = tf[k];  // register unit bit k (plan_rounds_wd)
+      const float2 tv = make_float2(-t, t);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if ((j >> k) & 1) continue;
+        const int w = j | (1 << k);
+        const float4 x = r[j], y = r[w];
+        const float2 x0 = bf_half(make_float2(x.x, x.y), make_float2(y.x, y.y), tv);
+        const float2 x1 = bf_half(make_float2(x.z, x.w), make_float2(y.z, y.w), tv);
+        const float2 y0 = bf_half(make_float2(y.x, y.y), make_float2(x.x, x.y), tv);
+        const float2 y1 = bf_half(make_float2(y.z, y.w), make_float2(x.z, x.w), tv);
+        r[j] = make_float4(x0.x, x0.y, x1.x, x1.y);
+        r[w] = make_float4(y0.x, y0.y, y1.x, y1.y);
+      }
+    }
+  }
+};
+
+template <int GK, int SK>
+__global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_constant__ SweepParams P) {
+  typedef WdSweep<GK, SK> W;
+  constexpr int MA = W::MA, MU = W::MU;
+  constexpr bool PH = W::PH;
+  constexpr int KA = kUnitBits + 1;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const unsigned smem_off = (1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u;
+  unsigned char* smem = smem_raw + smem_off;
+
+  const int n = P.n, q0 = P.q0, qU = q0 - 1;
+  const int nst = P.nstages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* stages = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * kWdStageBytes);
+  unsigned char* sp = smem + (size_t)nst * kWdStageBytes + 128;
+  double *Jm = nullptr, *Jx = nullptr;
+  if (PH) {
+    Jm = reinterpret_cast<double*>(sp);
+    Jx = Jm + n * n;
+    sp = smem + align16((size_t)(sp - smem) + 8 * (size_t)(n * n + n));
+  }
+  double* thr = reinterpret_cast<double*>(sp);  // [RA+1][kWdTT]
+  float2* PRR32 = reinterpret_cast<float2*>(thr + (kWdRA + 1) * kWdTT);
+  double* wsc = reinterpret_cast<double*>(PRR32 + 64);  // per team: hb[13], ebb
+  int* blk = reinterpret_cast<int*>(wsc + kWdTeams * 16);  // the block (non-tile) bits
+  int nb = 0;
+  for (int j = 0; j < n; ++j)
+    if (j >= MA && !(j >= q0 && j < q0 + KA - MA)) ++nb;
+
+  const int bl = qU - MU;  // block unit bits below the high run
+  if (threadIdx.x == 0) {
+    // full[stage][team]: each barrier has one consumer team that waits on it
+    // in order, so its parity (k / (nst * teams)) & 1 is never ambiguous
+    for (int s = 0; s < nst; ++s) {
+      for (int t = 0; t < kWdTeams; ++t) mbar_init(&full[s * kWdTeams + t], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (PH) {
+    for (int i = threadIdx.x; i < n * n; i += kWdThreads) Jm[i] = P.J.M[i];
+    for (int i = threadIdx.x; i < n; i += kWdThreads) Jx[i] = P.J.ext[i];
+    if (threadIdx.x == 0)
+      for (int j = 0, m = 0; j < n; ++j)
+        if (j >= MA && !(j >= q0 && j < q0 + KA - MA)) blk[m++] = j;
+  }
+  __syncthreads();
+  if (PH) {
+    // per tile-thread constants of the phase layout (L2): T_a (a < RA), E_TT
+    for (int tt = threadIdx.x; tt < kWdTT; tt += kWdThreads) {
+      for (int a = 0; a < kWdRA; ++a) {
+        const int ga = W::gpos(W::reg_bit(2, a), q0);
+        double acc = 0.0;
+        for (int j = 0; j < 7; ++j) {
+          const double w = Jm[ga * n + W::gpos(W::thr_bit(2, j), q0)];
+          acc += ((tt >> j) & 1) ? -w : w;
+        }
+        thr[a * kWdTT + tt] = acc;
+      }
+      double ett = 0.0;
+      for (int j = 0; j < 7; ++j) {
+        const int gj = W::gpos(W::thr_bit(2, j), q0);
+        const double sj = ((tt >> j) & 1) ? -1.0 : 1.0;
+        for (int j2 = j + 1; j2 < 7; ++j2) {
+          const double w = Jm[gj * n + W::gpos(W::thr_bit(2, j2), q0)];
+          ett += (((tt >> j2) & 1) ? -sj : sj) * w;
+        }
+      }
+      thr[kWdRA * kWdTT + tt] = ett;
+    }
+    for (int v = threadIdx.x; v < 64; v += kWdThreads) {
+      double acc = 0.0;
+      for (int a = 0; a < kWdRA; ++a) {
+        const int ga = W::gpos(W::reg_bit(2, a), q0);
+        const double sa = ((v >> a) & 1) ? -1.0 : 1.0;
+        for (int b = a + 1; b < kWdRA; ++b) {
+          const double w = Jm[ga * n + W::gpos(W::reg_bit(2, b), q0)];
+          acc += (((v >> b) & 1) ? -sa : sa) * w;
+        }
+      }
+      PRR32[v] = phasor32(acc);
+    }
+  }
+  __syncthreads();
+
+  Feed f;
+  f.tmap = &P.tmap;
+  f.stages = stages;
+  f.full = full;
+  f.nst = nst;
+  f.teams = 1;
+  f.bl = bl;
+  f.num_tiles = P.num_tiles;
+
+  // refill: the thread that stores a tile loads the tile nst steps ahead
+  // into its stage (no producer warp: 8 warps keep 255 registers)
+  auto feed = [&](int s, long long k) {
+    const long long tid = blockIdx.x + k * (long long)gridDim.x;
+    if (tid >= P.num_tiles) return;
+    void* dst = stages + (size_t)s * kWdStageBytes;
+    uint64_t* fb = &full[s * kWdTeams + (int)(k % kWdTeams)];
+    mbar_expect_tx(fb, kStageBytes);
+    const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
+    tma_load_5d(dst, f.tmap, fb, 0, 0, c1, 0, c4);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < nst; ++s) feed(s, s);
+
+
+  const int team = warp / kWdWarps, wq = warp % kWdWarps;
+  const int tt2 = wq | (lane << 2);  // tile-thread index in the phase layout (L2)
+  double* hb = wsc + team * 16;  // team: hb[0..12] fields, hb[15] block energy
+  float4* gamps = reinterpret_cast<float4*>(P.amps);
+  float4 r[32];
+
+  for (long long k = team;; k += kWdTeams) {
+    const long long tid = blockIdx.x + k * (long long)gridDim.x;
+    if (tid >= P.num_tiles) break;
+    const int s = (int)(k % nst);
+    float4* st = reinterpret_cast<float4*>(stages + (size_t)s * kWdStageBytes);
+    float4* rg = st + wq * kWdRegion;  // this warp's transpose region (after the team barrier)
+    const uint64_t ut = (uint64_t)tid;
+    const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
+
+    if constexpr (PH) {
+      // warp 0 of the team: per-tile fields on the tile bits from the fixed
+      // (block) bits and the block bits' own energy, for the whole team
+      // (read after the team barrier below)
+      if (wq == 0) {
+        const uint64_t base = baseU << 1;
+        if (lane < KA) {
+          const int gi = W::gpos(lane, q0);
+          double acc = Jx[gi];
+          for (int m = 0; m < nb; ++m) acc = fma(Jm[gi * n + blk[m]], spin(base, blk[m]), acc);
+          hb[lane] = acc;
+        }
+        double term = 0.0;
+        for (int m = lane; m < nb; m += 32) {
+          const int j = blk[m];
+          double fj = 0.0;
+          for (int m2 = 0; m2 < nb; ++m2) fj = fma(Jm[j * n + blk[m2]], spin(base, blk[m2]), fj);
+          term += spin(base, j) * (Jx[j] + 0.5 * fj);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+        if (lane == 0) hb[15] = P.J.cst + term;
+      }
+    }
+
+    mbar_wait(&full[s * kWdTeams + team], (unsigned)((k / (nst * kWdTeams)) & 1));
+    // L1: lane = unit bits 2..6, registers = unit bits 7..11 (natural layout)
+#pragma unroll
+    for (int b = 0; b < 32; ++b) r[b] = st[W::nat(wq, lane, b)];
+    if (!PH && !(P.scale_re == 1.0 && P.scale_im == 0.0)) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float2 a0 = cmul_amp(make_float2(r[j].x, r[j].y), make_double2(P.scale_re, P.scale_im));
+        const float2 a1 = cmul_amp(make_float2(r[j].z, r[j].w), make_double2(P.scale_re, P.scale_im));
+        r[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
+      }
+    }
+    W::template mix<31u>(r, P.tf[0][0]);
+    // the 4 warps of the tile have read the TMA layout: the stage is now
+    // split into per-warp transpose regions
+    team_sync_n(1 + team, kWdWarps * 32);
+#pragma unroll
+    for (int b = 0; b < 32; ++b) rg[W::slot(lane, b)] = r[b];
+    __syncwarp();
+    // L2: lane = unit bits 7..11, registers = unit bits 2..6
+#pragma unroll
+    for (int a = 0; a < 32; ++a) r[a] = rg[W::slot(a, lane)];
+    W::template mix<31u>(r, P.tf[0][1]);
+
+    if constexpr (PH) {
+      // phase in L2: E = C + sum_a s_a F_a + E_RR(v), v = (a << 1) | pair
+      double C = hb[15] + thr[kWdRA * kWdTT + tt2];
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        const double h = hb[W::thr_bit(2, j)];
+        C += ((tt2 >> j) & 1) ? -h : h;
+      }
+      float2 u[kWdRA];
+#pragma unroll
+      for (int a = 0; a < kWdRA; ++a) u[a] = phasor32(hb[W::reg_bit(2, a)] + thr[a * kWdTT + tt2]);
+      const float2 eC = cmul32(make_float2((float)P.scale_re, (float)P.scale_im), phasor32(C));
+      const float2 p01 = cmul32(u[0], u[1]), q01 = cmul32_conj(u[1], u[0]);
+      float2 Alo[4];
+      Alo[0] = cmul32(eC, p01);
+      Alo[1] = cmul32(eC, q01);
+      Alo[2] = cmul32_conj(eC, q01);
+      Alo[3] = cmul32_conj(eC, p01);
+      const float2 p23 = cmul32(u[2], u[3]), q23 = cmul32_conj(u[3], u[2]);
+      const float2 Y[4] = {p23, q23, conj32(q23), conj32(p23)};
+      const float2 p45 = cmul32(u[4], u[5]), q45 = cmul32_conj(u[5], u[4]);
+      const float2 Z[4] = {p45, q45, conj32(q45), conj32(p45)};
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        const float2 Bh = cmul32(Y[h & 3], Z[h >> 2]);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          const int v = h * 4 + l;
+          const float2 ph = cmul32(cmul32(Alo[l], Bh), PRR32[v]);
+          float4& q = r[v >> 1];
+          if (v & 1) {
+            const float2 x = cmul32(make_float2(q.z, q.w), ph);
+            q.z = x.x;
+            q.w = x.y;
+          } else {
+            const float2 x = cmul32(make_float2(q.x, q.y), ph);
+            q.x = x.x;
+            q.y = x.y;
+          }
+        }
+      }
+      W::template mix<31u>(r, P.tf[1][1]);
+    }
+    // back to L1 (conflict-free against the TMA layout) through the region
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < 32; ++a) rg[W::slot(a, lane)] = r[a];
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < 32; ++b) r[b] = rg[W::slot(lane, b)];
+    if constexpr (PH) W::template mix<31u>(r, P.tf[1][2]);
+    // every warp of the tile is past its region reads: write the tile back in
+    // the TMA layout and store it with one bulk tensor copy; the storing
+    // thread then refills the stage with the tile nst steps ahead
+    team_sync_n(1 + team, kWdWarps * 32);
+#pragma unroll
+    for (int b = 0; b < 32; ++b) st[W::nat(wq, lane, b)] = r[b];
+    fence_proxy_async();
+    team_sync_n(1 + team, kWdWarps * 32);
+    if (wq == kWdWarps - 1 && lane == 0) {  // warp 0 computes the next tile's fields
+      const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
+      tma_store_5d(f.tmap, st, 0, 0, c1, 0, c4);
+      bulk_commit();
+      bulk_wait_read<0>();
+      feed(s, k + nst);
+    }
+  }
+  if (lane == 0) bulk_wait<0>();  // stores complete before the kernel ends
+}
+
+}  // namespace lrq
