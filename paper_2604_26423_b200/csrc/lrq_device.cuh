@@ -136,22 +136,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware (up to
+// the hint, in ns) instead of spinning on issue slots the other warps need
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
   unsigned ok;
   asm volatile(
       "{\n .reg .pred p;\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
       " selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
+      : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
 // bounded wait: a lost transaction traps (a recoverable launch error) instead
-// of hanging the device
+// of hanging the device (each try_wait sleeps up to 1 ms: ~10^4 s in total)
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  for (unsigned long long i = 0; !mbar_try_wait(b, parity); ++i)
-    if (i > (1ull << 26)) __trap();
+  for (unsigned i = 0; !mbar_try_wait(b, parity); ++i)
+    if (i > (1u << 24)) __trap();
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2) {

@@ -407,13 +407,20 @@ int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
     return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
   sp.has_tmap = 1;
   sp.nstages = 3;
-  const size_t smem = wd_smem_bytes(sp.n, 3, sk == SK_F);
+  const size_t smem = wd_smem_bytes(sp.n, 3, sk == SK_F || sk == SK_P);
   if (smem > 227 * 1024) return fail(LRQ_ERUNTIME, "internal: warp-decoupled sweep needs too much shared memory");
   const int sms = sm_count(s->device);
   const int g = (int)(s->num_tiles < sms ? s->num_tiles : sms);
-  if (gk == GK_H) return sk == SK_F ? launch_wd_t<GK_H, SK_F>(s->stream, sp, g, smem)
-                                    : launch_wd_t<GK_H, SK_M>(s->stream, sp, g, smem);
-  return sk == SK_F ? launch_wd_t<GK_H4, SK_F>(s->stream, sp, g, smem) : launch_wd_t<GK_H4, SK_M>(s->stream, sp, g, smem);
+  const bool usesJ = sk == SK_F || sk == SK_P;
+  if (gk == GK_H) {
+    if (sk == SK_F) return launch_wd_t<GK_H, SK_F>(s->stream, sp, g, smem);
+    if (sk == SK_P) return launch_wd_t<GK_H, SK_P>(s->stream, sp, g, smem);
+    return launch_wd_t<GK_H, SK_M>(s->stream, sp, g, smem);
+  }
+  if (sk == SK_F) return launch_wd_t<GK_H4, SK_F>(s->stream, sp, g, smem);
+  if (sk == SK_P) return launch_wd_t<GK_H4, SK_P>(s->stream, sp, g, smem);
+  (void)usesJ;
+  return launch_wd_t<GK_H4, SK_M>(s->stream, sp, g, smem);
 }
 
 int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int grid) {

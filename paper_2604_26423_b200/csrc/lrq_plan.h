@@ -111,15 +111,19 @@ inline std::vector<PlanGroup> plan_groups(int n, int pair) {
 // F: L1 (mix1), L2 (mix1, phase, mix2), L1 (mix2).  Register amp bit a
 // (1..5) is tile amp bit (L1 ? 7 : 2) + a; bit 0 (the pair bit) is a run bit.
 // Its tangent goes to SweepParams::tf[w][r][a - 1].
-inline int wd_layout(int kind, int r) { return (kind == SK_F && r == 1) || (kind == SK_M && r == 1) ? 2 : 1; }
+// P (no load): L2 (phase, mix2), L1 (mix2).
+inline int wd_layout(int kind, int r) {
+  if (kind == SK_P) return r == 0 ? 2 : 1;
+  return (kind == SK_F && r == 1) || (kind == SK_M && r == 1) ? 2 : 1;
+}
 inline void plan_rounds_wd(const PlanGroup& g, PlanSweep& sw) {
-  sw.nrounds = sw.kind == SK_F ? 3 : 2;
+  sw.nrounds = sw.kind == SK_F ? 3 : 2;  // M, P: 2
   const unsigned targets[2] = {sw.target1 ? sw.target1 : g.tmask, g.tmask};
   if (!sw.ntarget1) sw.ntarget1 = sw.target1 ? __builtin_popcount(sw.target1) : g.ntargets;
   if (!sw.ntarget2) sw.ntarget2 = g.ntargets;
   for (int r = 0; r < sw.nrounds; ++r) {
     const int L = wd_layout(sw.kind, r);
-    const bool mixes[2] = {sw.kind == SK_M || r < 2, sw.kind == SK_F && r >= 1};
+    const bool mixes[2] = {sw.kind == SK_M || (sw.kind == SK_F && r < 2), (sw.kind == SK_F && r >= 1) || sw.kind == SK_P};
     unsigned m[2] = {0, 0}, tm[2] = {0, 0};
     for (int w = 0; w < 2; ++w)
       for (int a = 1; a <= 5; ++a) {
@@ -206,7 +210,7 @@ inline Plan make_plan(int n, int pair, int p) {
     const char* nowd = getenv("LRQ_NO_WD");  // debugging: classic kernels, same order
     auto wd = [&](int gi, int kind) {
       // F only: a lone high-group M (last layer) streams faster on the classic TMA kernel
-      return !(nowd && *nowd == '1') && P.groups[gi].kind != GK_A && kind == SK_F ? 1 : 0;
+      return !(nowd && *nowd == '1') && P.groups[gi].kind != GK_A && (kind == SK_F || kind == SK_P) ? 1 : 0;
     };
     auto push = [&](int gi, int kind, int b1, int ph, int b2, bool red) {
       PlanSweep w = make_sweep(gi, kind, b1, ph, b2, red);
@@ -336,8 +340,9 @@ inline std::string plan_json(const Plan& P) {
     for (int r = 0; r < w.nrounds; ++r) {
       s += (r ? "," : "");
       if (w.prog == 1) {  // lo: the lowest register unit bit of the layout
+        const bool ph = (w.kind == SK_F && r == 1) || (w.kind == SK_P && r == 0);
         s += "[" + std::to_string(wd_layout(w.kind, r) == 1 ? 7 : 2) + "," + std::to_string(w.tmask1[r]) + "," +
-             std::to_string(w.tmask2[r]) + "," + (w.kind == SK_F && r == 1 ? "1" : "0") + ",0]";
+             std::to_string(w.tmask2[r]) + "," + (ph ? "1" : "0") + ",0]";
         continue;
       }
       s += "[" + std::to_string(prog_lo(g.kind, P.pair, w.kind, r)) + "," + std::to_string(w.tmask1[r]) + "," +

@@ -59,7 +59,8 @@ struct WdSweep {
   static constexpr int MA = group_ma(GK, 1);  // run amp bits (3 or 4)
   static constexpr int MU = MA - 1;           // run unit bits (2 or 3)
   static constexpr int SWM = GK == GK_H ? 3 : 7;
-  static constexpr bool PH = SK == SK_F;
+  static constexpr bool PH = SK == SK_F || SK == SK_P;  // has a cost phase
+  static constexpr bool INIT = SK == SK_P;              // no load: H|0> value
 
   __device__ static __forceinline__ int swz(int e) { return e ^ ((e >> 3) & SWM); }
   // unit (a, b) of warp wq: natural TMA position / transposed slot
@@ -105,7 +106,8 @@ template <int GK, int SK>
 __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_constant__ SweepParams P) {
   typedef WdSweep<GK, SK> W;
   constexpr int MA = W::MA, MU = W::MU;
-  constexpr bool PH = W::PH;
+  constexpr bool PH = W::PH, INIT = W::INIT;
+  static_assert(SK == SK_M || SK == SK_F || SK == SK_P, "warp-decoupled sweeps: P, M, F");
   constexpr int KA = kUnitBits + 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const unsigned smem_off = (1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u;
@@ -196,25 +198,30 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
   f.num_tiles = P.num_tiles;
 
   // refill: the thread that stores a tile loads the tile nst steps ahead
-  // into its stage (no producer warp: 8 warps keep 255 registers)
+  // into its stage (no producer warp: 8 warps keep 255 registers).  P loads
+  // nothing: the same barrier then only says "stage free".
   auto feed = [&](int s, long long k) {
     const long long tid = blockIdx.x + k * (long long)gridDim.x;
     if (tid >= P.num_tiles) return;
-    void* dst = stages + (size_t)s * kWdStageBytes;
     uint64_t* fb = &full[s * kWdTeams + (int)(k % kWdTeams)];
-    mbar_expect_tx(fb, kStageBytes);
-    const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
-    tma_load_5d(dst, f.tmap, fb, 0, 0, c1, 0, c4);
+    if constexpr (INIT) {
+      mbar_arrive(fb);
+    } else {
+      void* dst = stages + (size_t)s * kWdStageBytes;
+      mbar_expect_tx(fb, kStageBytes);
+      const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
+      tma_load_5d(dst, f.tmap, fb, 0, 0, c1, 0, c4);
+    }
   };
   if (threadIdx.x == 0)
     for (int s = 0; s < nst; ++s) feed(s, s);
-
 
   const int team = warp / kWdWarps, wq = warp % kWdWarps;
   const int tt2 = wq | (lane << 2);  // tile-thread index in the phase layout (L2)
   double* hb = wsc + team * 16;  // team: hb[0..12] fields, hb[15] block energy
   float4* gamps = reinterpret_cast<float4*>(P.amps);
   float4 r[32];
+  constexpr int RPH = INIT ? 0 : 1;  // round of the phase / L2 layout
 
   for (long long k = team;; k += kWdTeams) {
     const long long tid = blockIdx.x + k * (long long)gridDim.x;
@@ -251,28 +258,32 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
     }
 
     mbar_wait(&full[s * kWdTeams + team], (unsigned)((k / (nst * kWdTeams)) & 1));
-    // L1: lane = unit bits 2..6, registers = unit bits 7..11 (natural layout)
+    if constexpr (!INIT) {
+      // L1: lane = unit bits 2..6, registers = unit bits 7..11 (TMA layout)
 #pragma unroll
-    for (int b = 0; b < 32; ++b) r[b] = st[W::nat(wq, lane, b)];
-    if (!PH && !(P.scale_re == 1.0 && P.scale_im == 0.0)) {
+      for (int b = 0; b < 32; ++b) r[b] = st[W::nat(wq, lane, b)];
+      if (!PH && !(P.scale_re == 1.0 && P.scale_im == 0.0)) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float2 a0 = cmul_amp(make_float2(r[j].x, r[j].y), make_double2(P.scale_re, P.scale_im));
-        const float2 a1 = cmul_amp(make_float2(r[j].z, r[j].w), make_double2(P.scale_re, P.scale_im));
-        r[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        for (int j = 0; j < 32; ++j) {
+          const float2 a0 = cmul_amp(make_float2(r[j].x, r[j].y), make_double2(P.scale_re, P.scale_im));
+          const float2 a1 = cmul_amp(make_float2(r[j].z, r[j].w), make_double2(P.scale_re, P.scale_im));
+          r[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        }
       }
+      W::template mix<31u>(r, P.tf[0][0]);
+      // the 4 warps of the tile have read the TMA layout: the stage is now
+      // split into per-warp transpose regions
+      team_sync_n(1 + team, kWdWarps * 32);
+#pragma unroll
+      for (int b = 0; b < 32; ++b) rg[W::slot(lane, b)] = r[b];
+      __syncwarp();
+      // L2: lane = unit bits 7..11, registers = unit bits 2..6
+#pragma unroll
+      for (int a = 0; a < 32; ++a) r[a] = rg[W::slot(a, lane)];
+      W::template mix<31u>(r, P.tf[0][1]);
+    } else {
+      team_sync_n(1 + team, kWdWarps * 32);  // warp 0's tile fields are visible
     }
-    W::template mix<31u>(r, P.tf[0][0]);
-    // the 4 warps of the tile have read the TMA layout: the stage is now
-    // split into per-warp transpose regions
-    team_sync_n(1 + team, kWdWarps * 32);
-#pragma unroll
-    for (int b = 0; b < 32; ++b) rg[W::slot(lane, b)] = r[b];
-    __syncwarp();
-    // L2: lane = unit bits 7..11, registers = unit bits 2..6
-#pragma unroll
-    for (int a = 0; a < 32; ++a) r[a] = rg[W::slot(a, lane)];
-    W::template mix<31u>(r, P.tf[0][1]);
 
     if constexpr (PH) {
       // phase in L2: E = C + sum_a s_a F_a + E_RR(v), v = (a << 1) | pair
@@ -285,7 +296,9 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       float2 u[kWdRA];
 #pragma unroll
       for (int a = 0; a < kWdRA; ++a) u[a] = phasor32(hb[W::reg_bit(2, a)] + thr[a * kWdTT + tt2]);
-      const float2 eC = cmul32(make_float2((float)P.scale_re, (float)P.scale_im), phasor32(C));
+      double2 sc = make_double2(P.scale_re, P.scale_im);
+      if constexpr (INIT) sc = cmul(sc, make_double2(P.init_re, P.init_im));
+      const float2 eC = cmul32(make_float2((float)sc.x, (float)sc.y), phasor32(C));
       const float2 p01 = cmul32(u[0], u[1]), q01 = cmul32_conj(u[1], u[0]);
       float2 Alo[4];
       Alo[0] = cmul32(eC, p01);
@@ -304,18 +317,17 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
           const int v = h * 4 + l;
           const float2 ph = cmul32(cmul32(Alo[l], Bh), PRR32[v]);
           float4& q = r[v >> 1];
+          const float2 x = INIT ? ph : cmul32((v & 1) ? make_float2(q.z, q.w) : make_float2(q.x, q.y), ph);
           if (v & 1) {
-            const float2 x = cmul32(make_float2(q.z, q.w), ph);
             q.z = x.x;
             q.w = x.y;
           } else {
-            const float2 x = cmul32(make_float2(q.x, q.y), ph);
             q.x = x.x;
             q.y = x.y;
           }
         }
       }
-      W::template mix<31u>(r, P.tf[1][1]);
+      W::template mix<31u>(r, P.tf[1][RPH]);
     }
     // back to L1 (conflict-free against the TMA layout) through the region
     __syncwarp();
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
     __syncwarp();
 #pragma unroll
     for (int b = 0; b < 32; ++b) r[b] = rg[W::slot(lane, b)];
-    if constexpr (PH) W::template mix<31u>(r, P.tf[1][2]);
+    if constexpr (PH) W::template mix<31u>(r, P.tf[1][RPH + 1]);
     // every warp of the tile is past its region reads: write the tile back in
     // the TMA layout and store it with one bulk tensor copy; the storing
     // thread then refills the stage with the tile nst steps ahead

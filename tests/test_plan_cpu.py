@@ -148,7 +148,7 @@ def test_plan_structure(lib, n, pb):
             # layout of group A; H layouts keep register units above the run)
             if sw.get("prog") == 1:
                 # warp-decoupled high-group sweep: TMA in, complex64 only
-                assert g["kind"] != "A" and pair == 1 and sw["kind"] in "MF"
+                assert g["kind"] != "A" and pair == 1 and sw["kind"] in "PMF"
                 continue
             for lo in {sw["rounds"][-1][0], sw["rounds"][0][0]}:
                 if g["kind"] == "A":
