@@ -384,25 +384,32 @@ bool use_tma_path(int pbytes, int gk, int sk) {
   return pbytes == 8 && gk != GK_A && (sk == SK_M || sk == SK_F);
 }
 
-template <int GK, int SK>
+template <typename T, int GK, int SK>
 int launch_wd_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(sweep_wd_kernel<GK, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    err = cudaFuncSetAttribute(sweep_wd_kernel<T, GK, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   CUDA_TRY(err);
-  sweep_wd_kernel<GK, SK><<<grid, kWdThreads, smem, st>>>(sp);
+  sweep_wd_kernel<T, GK, SK><<<grid, kWdThreads, smem, st>>>(sp);
   CUDA_TRY(cudaGetLastError());
   return LRQ_OK;
 }
 
-// warp-decoupled complex64 high-group sweep (plan prog 1): TMA ring of 3
-// stages, 2 tiles in flight, one CTA per SM
+template <typename T, int GK>
+int launch_wd_kind(cudaStream_t st, int sk, const SweepParams& sp, int grid, size_t smem) {
+  if (sk == SK_F) return launch_wd_t<T, GK, SK_F>(st, sp, grid, smem);
+  if (sk == SK_P) return launch_wd_t<T, GK, SK_P>(st, sp, grid, smem);
+  return launch_wd_t<T, GK, SK_M>(st, sp, grid, smem);
+}
+
+// warp-decoupled high-group sweep (plan prog 1): TMA ring of 3 stages, 2
+// tiles in flight, one CTA per SM
 int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
   SweepParams sp = sp_in;
   const int K = tile_amp_bits(s->pbytes);
-  const int ma = group_ma(gk, 1);
+  const int ma = group_ma(gk, pair_of(s->pbytes));
   if (!make_tile_tmap(&sp.tmap, s->amps, gk, sp.n, s->pbytes, ma, K, sp.q0, s->num_tiles))
     return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
   sp.has_tmap = 1;
@@ -411,16 +418,12 @@ int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
   if (smem > 227 * 1024) return fail(LRQ_ERUNTIME, "internal: warp-decoupled sweep needs too much shared memory");
   const int sms = sm_count(s->device);
   const int g = (int)(s->num_tiles < sms ? s->num_tiles : sms);
-  const bool usesJ = sk == SK_F || sk == SK_P;
-  if (gk == GK_H) {
-    if (sk == SK_F) return launch_wd_t<GK_H, SK_F>(s->stream, sp, g, smem);
-    if (sk == SK_P) return launch_wd_t<GK_H, SK_P>(s->stream, sp, g, smem);
-    return launch_wd_t<GK_H, SK_M>(s->stream, sp, g, smem);
+  if (s->pbytes == 16) {
+    if (gk != GK_H) return fail(LRQ_ERUNTIME, "internal: complex128 warp-decoupled sweeps need an H group");
+    return launch_wd_kind<double, GK_H>(s->stream, sk, sp, g, smem);
   }
-  if (sk == SK_F) return launch_wd_t<GK_H4, SK_F>(s->stream, sp, g, smem);
-  if (sk == SK_P) return launch_wd_t<GK_H4, SK_P>(s->stream, sp, g, smem);
-  (void)usesJ;
-  return launch_wd_t<GK_H4, SK_M>(s->stream, sp, g, smem);
+  if (gk == GK_H) return launch_wd_kind<float, GK_H>(s->stream, sk, sp, g, smem);
+  return launch_wd_kind<float, GK_H4>(s->stream, sk, sp, g, smem);
 }
 
 int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int grid) {

@@ -106,17 +106,16 @@ inline std::vector<PlanGroup> plan_groups(int n, int pair) {
 // register bit that is not one of the group's targets gets tangent 0.
 // mask*[r] = register amp bits that take a real butterfly in round r,
 // tmask*[r] = the same bits as tile amp bits.
-// warp-decoupled program (complex64 H/H4, M and F sweeps): layout L1 holds
-// tile amp bits 8..12 in registers, L2 bits 3..7; rounds M: L1, L2;
-// F: L1 (mix1), L2 (mix1, phase, mix2), L1 (mix2).  Register amp bit a
-// (1..5) is tile amp bit (L1 ? 7 : 2) + a; bit 0 (the pair bit) is a run bit.
-// Its tangent goes to SweepParams::tf[w][r][a - 1].
+// warp-decoupled program (high groups; P, M, F sweeps): layout L1 holds tile
+// unit bits 7..11 in registers, L2 unit bits 2..6; rounds M: L1, L2;
+// F: L1 (mix1), L2 (mix1, phase, mix2), L1 (mix2).  Register unit bit k
+// (tile amp bit (L1 ? 7 : 2) + k + pair) takes tangent SweepParams::tf[w][r][k].
 // P (no load): L2 (phase, mix2), L1 (mix2).
 inline int wd_layout(int kind, int r) {
   if (kind == SK_P) return r == 0 ? 2 : 1;
   return (kind == SK_F && r == 1) || (kind == SK_M && r == 1) ? 2 : 1;
 }
-inline void plan_rounds_wd(const PlanGroup& g, PlanSweep& sw) {
+inline void plan_rounds_wd(const PlanGroup& g, int pair, PlanSweep& sw) {
   sw.nrounds = sw.kind == SK_F ? 3 : 2;  // M, P: 2
   const unsigned targets[2] = {sw.target1 ? sw.target1 : g.tmask, g.tmask};
   if (!sw.ntarget1) sw.ntarget1 = sw.target1 ? __builtin_popcount(sw.target1) : g.ntargets;
@@ -126,10 +125,10 @@ inline void plan_rounds_wd(const PlanGroup& g, PlanSweep& sw) {
     const bool mixes[2] = {sw.kind == SK_M || (sw.kind == SK_F && r < 2), (sw.kind == SK_F && r >= 1) || sw.kind == SK_P};
     unsigned m[2] = {0, 0}, tm[2] = {0, 0};
     for (int w = 0; w < 2; ++w)
-      for (int a = 1; a <= 5; ++a) {
-        const unsigned tb = 1u << ((L == 1 ? 7 : 2) + a);
+      for (int k = 0; k < 5; ++k) {  // register unit bit k = unit bit (L1 ? 7 : 2) + k
+        const unsigned tb = 1u << ((L == 1 ? 7 : 2) + k + pair);
         if (mixes[w] && (targets[w] & tb)) {
-          m[w] |= 1u << (a - 1);  // tangent slot k = a - 1 (the pair bit never mixes)
+          m[w] |= 1u << k;  // tangent slot k (the complex64 pair bit never mixes)
           tm[w] |= tb;
         }
       }
@@ -142,7 +141,7 @@ inline void plan_rounds_wd(const PlanGroup& g, PlanSweep& sw) {
 
 inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
   if (sw.prog == 1) {
-    plan_rounds_wd(g, sw);
+    plan_rounds_wd(g, pair, sw);
     return;
   }
   const int RA = 4 + pair;
@@ -196,9 +195,9 @@ inline Plan make_plan(int n, int pair, int p) {
   if (P.small || p < 1) return P;
   P.groups = plan_groups(n, pair);
   const int S = (int)P.groups.size();
-  if (pair && S >= 3) {
-    // complex64 with >= 2 high groups: the fused F sweeps go to the two end
-    // HIGH groups (warp-decoupled kernel, two transposes), group A sits in
+  if (S >= 3) {
+    // >= 2 high groups: the fused F sweeps go to the two end HIGH groups
+    // (warp-decoupled kernel, two transposes), group A sits in
     // the middle (M sweeps) and takes the final reduction: the last layer
     // visits its remaining groups with A last.
     //   order  E1=G_1, mids = A, G_2..G_{S-2}, E2 = G_{S-1}

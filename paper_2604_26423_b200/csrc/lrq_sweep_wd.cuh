@@ -1,14 +1,14 @@
-// Warp-decoupled sweeps of a complex64 high qubit group (H: 64 B runs, H4:
-// 128 B runs), for the mixer-only (M) and the fused mix -> phase -> mix (F)
-// sweeps.  DESIGN.md §3.2.
+// Warp-decoupled sweeps of a high qubit group (complex64 H: 64 B runs, H4:
+// 128 B runs; complex128 H: 256 B runs) for the first (P), mixer-only (M)
+// and fused mix -> phase -> mix (F) sweeps.  DESIGN.md §3.2.
 //
 // A high-group tile is 2^(KA-MA) runs of 2^MA contiguous amplitudes; the run
 // bits are NOT mixer targets in this sweep.  Unit bits 0-1 of the tile (inside
 // every run) therefore never need a butterfly, and they pick the warp: each
 // of the tile's 4 warps owns the 1024 units with its value of those bits and
 // exchanges no data with the other three.  Inside a warp the 10 remaining
-// unit bits are split 5 lanes x 5 registers (32 float4 units = 64 amplitudes
-// per thread), so two layouts cover every target:
+// unit bits are split 5 lanes x 5 registers (32 16-byte units per thread: 64
+// complex64 or 32 complex128 amplitudes), so two layouts cover every target:
 //     L1: lane = unit bits 2..6, registers = unit bits 7..11
 //     L2: lane = unit bits 7..11, registers = unit bits 2..6
 // M = L1 mix, L2 mix; F = L1 mix1, L2 mix1 + phase + mix2, L1 mix2.  Both
@@ -22,8 +22,9 @@
 // pair brackets the write-back in the TMA layout, one thread issues the TMA
 // tensor store, waits for it to have read the stage, and loads the tile nst
 // steps ahead into it.  Two tiles are in flight per CTA (8 warps, 2 per SM
-// sub-partition, which keeps 255 registers for the 64 amplitudes a thread
-// holds); the two teams run out of phase.
+// sub-partition, which keeps 255 registers for the 32 units a thread holds);
+// the two teams run out of phase.  P starts from the H|0> value in L2 and
+// loads nothing.
 //
 // Bank conflicts: the TMA swizzle puts unit e at e ^ ((e >> 3) & SWM); L1
 // accesses of the TMA layout have lanes on unit bits 2..4 -> 8 distinct
@@ -37,7 +38,7 @@ constexpr int kWdTeams = 2;  // tiles in flight per CTA
 constexpr int kWdWarps = 4;  // warps per tile
 constexpr int kWdThreads = kWdTeams * kWdWarps * 32;  // no producer warp (see refill)
 constexpr int kWdTT = kWdWarps * 32;  // tile threads
-constexpr int kWdRA = 6;              // register amp bits: pair + 5 unit bits
+constexpr int kWdRAmax = 6;           // register amp bits: (pair) + 5 unit bits
 // a stage holds the 64 KB TMA tile plus 2 KB so that, after the tile is read,
 // each warp owns a padded 32 x 33-unit transpose region of it
 constexpr int kWdStageBytes = 66 * 1024;
@@ -46,19 +47,24 @@ constexpr int kWdRegion = 32 * 33;  // units per warp region
 __host__ __device__ inline size_t wd_smem_bytes(int n, int nst, bool usesJ) {
   size_t b = (size_t)nst * kWdStageBytes + 128;  // stages + full barriers
   if (usesJ) b = align16(b + 8 * (size_t)(n * n + n));
-  b += 8 * (size_t)((kWdRA + 1) * kWdTT);  // per-tile-thread constants
-  b += 8 * 64;                             // PRR32 (float2 x 64)
+  b += 8 * (size_t)((kWdRAmax + 1) * kWdTT);  // per-tile-thread constants
+  b += 16 * 64;                               // PRR (float2 x 64 or double2 x 32)
   b += 8 * (size_t)(kWdTeams * 16);  // per-team hb[13] + ebb
   b += 4 * 64;                         // block-bit list
   return align16(b) + 1024;
 }
 
-template <int GK, int SK>
+template <typename T, int GK, int SK>
 struct WdSweep {
-  static_assert(GK == GK_H || GK == GK_H4, "warp-decoupled sweeps serve complex64 high groups");
-  static constexpr int MA = group_ma(GK, 1);  // run amp bits (3 or 4)
-  static constexpr int MU = MA - 1;           // run unit bits (2 or 3)
-  static constexpr int SWM = GK == GK_H ? 3 : 7;
+  typedef typename UnitT<T>::U U;
+  static constexpr int PAIR = UnitT<T>::PAIR;
+  static_assert(GK == GK_H || (GK == GK_H4 && PAIR), "warp-decoupled sweeps serve high groups");
+  static constexpr int KA = kUnitBits + PAIR;
+  static constexpr int RA = 5 + PAIR;         // register amp bits
+  static constexpr int NV = 1 << RA;          // amplitudes per thread
+  static constexpr int MA = group_ma(GK, PAIR);  // run amp bits
+  static constexpr int MU = MA - PAIR;           // run unit bits (>= 2)
+  static constexpr int SWM = (GK == GK_H && PAIR) ? 3 : 7;
   static constexpr bool PH = SK == SK_F || SK == SK_P;  // has a cost phase
   static constexpr bool INIT = SK == SK_P;              // no load: H|0> value
 
@@ -69,18 +75,22 @@ struct WdSweep {
   // to 33 units -> bank group (a + b) & 7, conflict-free for a lane-a writer
   // and a lane-b reader, and base + immediate addressing both ways
   __device__ static __forceinline__ int slot(int a, int b) { return a * 33 + b; }
-  // tile amp bit of register amp bit r (0 = pair) in layout L (1: regs = unit
-  // bits 7..11, 2: regs = unit bits 2..6)
-  __host__ __device__ static constexpr int reg_bit(int L, int r) { return r == 0 ? 0 : (L == 1 ? 7 : 2) + r; }
-  // tile amp bit of tile-thread bit j (warp bits 0-1, then the 5 lane bits)
-  __host__ __device__ static constexpr int thr_bit(int L, int j) { return j < 2 ? 1 + j : (L == 1 ? 3 : 8) + (j - 2); }
+  // tile amp bit of register amp bit r in layout L (1: regs = unit bits
+  // 7..11, 2: regs = unit bits 2..6); complex64: r = 0 is the pair bit
+  __host__ __device__ static constexpr int reg_bit(int L, int r) {
+    return PAIR ? (r == 0 ? 0 : (L == 1 ? 7 : 2) + r) : (L == 1 ? 7 : 2) + r;
+  }
+  // tile amp bit of tile-thread bit j (warp bits = unit bits 0-1, then the 5
+  // lane bits)
+  __host__ __device__ static constexpr int thr_bit(int L, int j) {
+    return PAIR + (j < 2 ? j : (L == 1 ? 2 : 7) + (j - 2));
+  }
 
   __device__ static __forceinline__ int gpos(int i, int q0) { return i < MA ? i : q0 + (i - MA); }
 
-  // butterflies on register unit bits of MASK (x + i t y, y + i t x) on both
-  // amplitudes of each unit
+  // butterflies on register unit bits of MASK: (x, y) <- (x + i t y, y + i t x)
   template <unsigned MASK>
-  __device__ static __forceinline__ void mix(float4 (&r)[32], const float* tf) {
+  __device__ static __forceinline__ void mix(float4 (&r)[32], const float* tf, const double*) {
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       if (!((MASK >> k) & 1u)) continue;
@@ -100,20 +110,114 @@ struct WdSweep {
       }
     }
   }
+  template <unsigned MASK>
+  __device__ static __forceinline__ void mix(double2 (&r)[32], const float*, const double* td) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (!((MASK >> k) & 1u)) continue;
+      const double t = td[k];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if ((j >> k) & 1) continue;
+        const int w = j | (1 << k);
+        const double2 x = r[j], y = r[w];
+        r[j] = bf_half(x, y, t);
+        r[w] = bf_half(y, x, t);
+      }
+    }
+  }
+  // per-amplitude access of the register file (v: register amp index)
+  __device__ static __forceinline__ float2 get(const float4 (&r)[32], int v) {
+    return (v & 1) ? make_float2(r[v >> 1].z, r[v >> 1].w) : make_float2(r[v >> 1].x, r[v >> 1].y);
+  }
+  __device__ static __forceinline__ void set(float4 (&r)[32], int v, float2 a) {
+    if (v & 1) {
+      r[v >> 1].z = a.x;
+      r[v >> 1].w = a.y;
+    } else {
+      r[v >> 1].x = a.x;
+      r[v >> 1].y = a.y;
+    }
+  }
+  __device__ static __forceinline__ double2 get(const double2 (&r)[32], int v) { return r[v]; }
+  __device__ static __forceinline__ void set(double2 (&r)[32], int v, double2 a) { r[v] = a; }
+  __device__ static __forceinline__ void scale_all(float4 (&r)[32], double2 sc) {
+#pragma unroll
+    for (int v = 0; v < 64; ++v) set(r, v, cmul_amp(get(r, v), sc));
+  }
+  __device__ static __forceinline__ void scale_all(double2 (&r)[32], double2 sc) {
+#pragma unroll
+    for (int v = 0; v < 32; ++v) r[v] = cmul(r[v], sc);
+  }
+
+  // cost phase in L2: amplitude v *= sc * exp(-i (C + sum_a s_a F_a + E_RR(v)))
+  // (INIT: amplitude v = that phasor); product form as in SweepTile::phase
+  __device__ static __forceinline__ void phase(float4 (&r)[32], double C, const double* F, double2 sc,
+                                               const void* prr) {
+    const float2* PRR32 = reinterpret_cast<const float2*>(prr);
+    float2 u[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) u[a] = phasor32(F[a]);
+    const float2 eC = cmul32(make_float2((float)sc.x, (float)sc.y), phasor32(C));
+    const float2 p01 = cmul32(u[0], u[1]), q01 = cmul32_conj(u[1], u[0]);
+    float2 Alo[4];
+    Alo[0] = cmul32(eC, p01);
+    Alo[1] = cmul32(eC, q01);
+    Alo[2] = cmul32_conj(eC, q01);
+    Alo[3] = cmul32_conj(eC, p01);
+    const float2 p23 = cmul32(u[2], u[3]), q23 = cmul32_conj(u[3], u[2]);
+    const float2 Y[4] = {p23, q23, conj32(q23), conj32(p23)};
+    const float2 p45 = cmul32(u[4], u[5]), q45 = cmul32_conj(u[5], u[4]);
+    const float2 Z[4] = {p45, q45, conj32(q45), conj32(p45)};
+#pragma unroll
+    for (int h = 0; h < 16; ++h) {
+      const float2 Bh = cmul32(Y[h & 3], Z[h >> 2]);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const int v = h * 4 + l;
+        const float2 ph = cmul32(cmul32(Alo[l], Bh), PRR32[v]);
+        set(r, v, INIT ? ph : cmul32(get(r, v), ph));
+      }
+    }
+  }
+  __device__ static __forceinline__ void phase(double2 (&r)[32], double C, const double* F, double2 sc,
+                                               const void* prr) {
+    const double2* PRR = reinterpret_cast<const double2*>(prr);
+    const double2 eC = cmul(sc, expmi(C));
+    const double2 u0 = expmi(F[0]), u1 = expmi(F[1]), u2 = expmi(F[2]), u3 = expmi(F[3]), u4 = expmi(F[4]);
+    const double2 p01 = cmul(u0, u1), q01 = cmul_conj(u1, u0);
+    double2 Alo[4];
+    Alo[0] = cmul(eC, p01);
+    Alo[1] = cmul(eC, q01);
+    Alo[2] = cmul_conj(eC, q01);
+    Alo[3] = cmul_conj(eC, p01);
+    const double2 p23 = cmul(u2, u3), q23 = cmul_conj(u3, u2);
+    const double2 Y[4] = {p23, q23, make_double2(q23.x, -q23.y), make_double2(p23.x, -p23.y)};
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const double2 Bh = (h & 4) ? cmul_conj(Y[h & 3], u4) : cmul(Y[h & 3], u4);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const int v = h * 4 + l;
+        const double2 ph = cmul(cmul(Alo[l], Bh), PRR[v]);
+        r[v] = INIT ? ph : cmul(r[v], ph);
+      }
+    }
+  }
 };
 
-template <int GK, int SK>
+template <typename T, int GK, int SK>
 __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_constant__ SweepParams P) {
-  typedef WdSweep<GK, SK> W;
-  constexpr int MA = W::MA, MU = W::MU;
+  typedef WdSweep<T, GK, SK> W;
+  typedef typename W::U U;
+  constexpr int MA = W::MA, MU = W::MU, KA = W::KA, RA = W::RA, NV = W::NV, PAIR = W::PAIR;
   constexpr bool PH = W::PH, INIT = W::INIT;
   static_assert(SK == SK_M || SK == SK_F || SK == SK_P, "warp-decoupled sweeps: P, M, F");
-  constexpr int KA = kUnitBits + 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const unsigned smem_off = (1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u;
   unsigned char* smem = smem_raw + smem_off;
 
-  const int n = P.n, q0 = P.q0, qU = q0 - 1;
+  const int n = P.n, q0 = P.q0, qU = q0 - PAIR;
   const int nst = P.nstages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* stages = smem;
@@ -125,9 +229,9 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
     Jx = Jm + n * n;
     sp = smem + align16((size_t)(sp - smem) + 8 * (size_t)(n * n + n));
   }
-  double* thr = reinterpret_cast<double*>(sp);  // [RA+1][kWdTT]
-  float2* PRR32 = reinterpret_cast<float2*>(thr + (kWdRA + 1) * kWdTT);
-  double* wsc = reinterpret_cast<double*>(PRR32 + 64);  // per team: hb[13], ebb
+  double* thr = reinterpret_cast<double*>(sp);                          // [RA+1][kWdTT]
+  void* PRR = reinterpret_cast<void*>(thr + (kWdRAmax + 1) * kWdTT);  // NV phasors
+  double* wsc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(PRR) + 16 * 64);  // per team
   int* blk = reinterpret_cast<int*>(wsc + kWdTeams * 16);  // the block (non-tile) bits
   int nb = 0;
   for (int j = 0; j < n; ++j)
@@ -137,9 +241,8 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
   if (threadIdx.x == 0) {
     // full[stage][team]: each barrier has one consumer team that waits on it
     // in order, so its parity (k / (nst * teams)) & 1 is never ambiguous
-    for (int s = 0; s < nst; ++s) {
+    for (int s = 0; s < nst; ++s)
       for (int t = 0; t < kWdTeams; ++t) mbar_init(&full[s * kWdTeams + t], 1);
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (PH) {
@@ -153,7 +256,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
   if (PH) {
     // per tile-thread constants of the phase layout (L2): T_a (a < RA), E_TT
     for (int tt = threadIdx.x; tt < kWdTT; tt += kWdThreads) {
-      for (int a = 0; a < kWdRA; ++a) {
+      for (int a = 0; a < RA; ++a) {
         const int ga = W::gpos(W::reg_bit(2, a), q0);
         double acc = 0.0;
         for (int j = 0; j < 7; ++j) {
@@ -171,31 +274,23 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
           ett += (((tt >> j2) & 1) ? -sj : sj) * w;
         }
       }
-      thr[kWdRA * kWdTT + tt] = ett;
+      thr[RA * kWdTT + tt] = ett;
     }
-    for (int v = threadIdx.x; v < 64; v += kWdThreads) {
+    for (int v = threadIdx.x; v < NV; v += kWdThreads) {
       double acc = 0.0;
-      for (int a = 0; a < kWdRA; ++a) {
+      for (int a = 0; a < RA; ++a) {
         const int ga = W::gpos(W::reg_bit(2, a), q0);
         const double sa = ((v >> a) & 1) ? -1.0 : 1.0;
-        for (int b = a + 1; b < kWdRA; ++b) {
+        for (int b = a + 1; b < RA; ++b) {
           const double w = Jm[ga * n + W::gpos(W::reg_bit(2, b), q0)];
           acc += (((v >> b) & 1) ? -sa : sa) * w;
         }
       }
-      PRR32[v] = phasor32(acc);
+      if (PAIR) reinterpret_cast<float2*>(PRR)[v] = phasor32(acc);
+      else reinterpret_cast<double2*>(PRR)[v] = expmi(acc);
     }
   }
   __syncthreads();
-
-  Feed f;
-  f.tmap = &P.tmap;
-  f.stages = stages;
-  f.full = full;
-  f.nst = nst;
-  f.teams = 1;
-  f.bl = bl;
-  f.num_tiles = P.num_tiles;
 
   // refill: the thread that stores a tile loads the tile nst steps ahead
   // into its stage (no producer warp: 8 warps keep 255 registers).  P loads
@@ -210,7 +305,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       void* dst = stages + (size_t)s * kWdStageBytes;
       mbar_expect_tx(fb, kStageBytes);
       const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
-      tma_load_5d(dst, f.tmap, fb, 0, 0, c1, 0, c4);
+      tma_load_5d(dst, &P.tmap, fb, 0, 0, c1, 0, c4);
     }
   };
   if (threadIdx.x == 0)
@@ -218,17 +313,18 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
 
   const int team = warp / kWdWarps, wq = warp % kWdWarps;
   const int tt2 = wq | (lane << 2);  // tile-thread index in the phase layout (L2)
-  double* hb = wsc + team * 16;  // team: hb[0..12] fields, hb[15] block energy
-  float4* gamps = reinterpret_cast<float4*>(P.amps);
-  float4 r[32];
+  double* hb = wsc + team * 16;      // team: hb[0..KA-1] fields, hb[15] block energy
+  U* gamps = reinterpret_cast<U*>(P.amps);
+  U r[32];
   constexpr int RPH = INIT ? 0 : 1;  // round of the phase / L2 layout
+  const double2 scale = make_double2(P.scale_re, P.scale_im);
 
   for (long long k = team;; k += kWdTeams) {
     const long long tid = blockIdx.x + k * (long long)gridDim.x;
     if (tid >= P.num_tiles) break;
     const int s = (int)(k % nst);
-    float4* st = reinterpret_cast<float4*>(stages + (size_t)s * kWdStageBytes);
-    float4* rg = st + wq * kWdRegion;  // this warp's transpose region (after the team barrier)
+    U* st = reinterpret_cast<U*>(stages + (size_t)s * kWdStageBytes);
+    U* rg = st + wq * kWdRegion;  // this warp's transpose region (after the team barrier)
     const uint64_t ut = (uint64_t)tid;
     const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
 
@@ -237,7 +333,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       // (block) bits and the block bits' own energy, for the whole team
       // (read after the team barrier below)
       if (wq == 0) {
-        const uint64_t base = baseU << 1;
+        const uint64_t base = baseU << PAIR;
         if (lane < KA) {
           const int gi = W::gpos(lane, q0);
           double acc = Jx[gi];
@@ -262,15 +358,8 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       // L1: lane = unit bits 2..6, registers = unit bits 7..11 (TMA layout)
 #pragma unroll
       for (int b = 0; b < 32; ++b) r[b] = st[W::nat(wq, lane, b)];
-      if (!PH && !(P.scale_re == 1.0 && P.scale_im == 0.0)) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float2 a0 = cmul_amp(make_float2(r[j].x, r[j].y), make_double2(P.scale_re, P.scale_im));
-          const float2 a1 = cmul_amp(make_float2(r[j].z, r[j].w), make_double2(P.scale_re, P.scale_im));
-          r[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
-        }
-      }
-      W::template mix<31u>(r, P.tf[0][0]);
+      if (!PH && !(scale.x == 1.0 && scale.y == 0.0)) W::scale_all(r, scale);
+      W::template mix<31u>(r, P.tf[0][0], P.td[0][0]);
       // the 4 warps of the tile have read the TMA layout: the stage is now
       // split into per-warp transpose regions
       team_sync_n(1 + team, kWdWarps * 32);
@@ -280,54 +369,25 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       // L2: lane = unit bits 7..11, registers = unit bits 2..6
 #pragma unroll
       for (int a = 0; a < 32; ++a) r[a] = rg[W::slot(a, lane)];
-      W::template mix<31u>(r, P.tf[0][1]);
+      W::template mix<31u>(r, P.tf[0][1], P.td[0][1]);
     } else {
       team_sync_n(1 + team, kWdWarps * 32);  // warp 0's tile fields are visible
     }
 
     if constexpr (PH) {
-      // phase in L2: E = C + sum_a s_a F_a + E_RR(v), v = (a << 1) | pair
-      double C = hb[15] + thr[kWdRA * kWdTT + tt2];
+      // phase in L2: E = C + sum_a s_a F_a + E_RR(v)
+      double C = hb[15] + thr[RA * kWdTT + tt2];
 #pragma unroll
       for (int j = 0; j < 7; ++j) {
         const double h = hb[W::thr_bit(2, j)];
         C += ((tt2 >> j) & 1) ? -h : h;
       }
-      float2 u[kWdRA];
+      double F[RA];
 #pragma unroll
-      for (int a = 0; a < kWdRA; ++a) u[a] = phasor32(hb[W::reg_bit(2, a)] + thr[a * kWdTT + tt2]);
-      double2 sc = make_double2(P.scale_re, P.scale_im);
-      if constexpr (INIT) sc = cmul(sc, make_double2(P.init_re, P.init_im));
-      const float2 eC = cmul32(make_float2((float)sc.x, (float)sc.y), phasor32(C));
-      const float2 p01 = cmul32(u[0], u[1]), q01 = cmul32_conj(u[1], u[0]);
-      float2 Alo[4];
-      Alo[0] = cmul32(eC, p01);
-      Alo[1] = cmul32(eC, q01);
-      Alo[2] = cmul32_conj(eC, q01);
-      Alo[3] = cmul32_conj(eC, p01);
-      const float2 p23 = cmul32(u[2], u[3]), q23 = cmul32_conj(u[3], u[2]);
-      const float2 Y[4] = {p23, q23, conj32(q23), conj32(p23)};
-      const float2 p45 = cmul32(u[4], u[5]), q45 = cmul32_conj(u[5], u[4]);
-      const float2 Z[4] = {p45, q45, conj32(q45), conj32(p45)};
-#pragma unroll
-      for (int h = 0; h < 16; ++h) {
-        const float2 Bh = cmul32(Y[h & 3], Z[h >> 2]);
-#pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const int v = h * 4 + l;
-          const float2 ph = cmul32(cmul32(Alo[l], Bh), PRR32[v]);
-          float4& q = r[v >> 1];
-          const float2 x = INIT ? ph : cmul32((v & 1) ? make_float2(q.z, q.w) : make_float2(q.x, q.y), ph);
-          if (v & 1) {
-            q.z = x.x;
-            q.w = x.y;
-          } else {
-            q.x = x.x;
-            q.y = x.y;
-          }
-        }
-      }
-      W::template mix<31u>(r, P.tf[1][RPH]);
+      for (int a = 0; a < RA; ++a) F[a] = hb[W::reg_bit(2, a)] + thr[a * kWdTT + tt2];
+      const double2 sc = INIT ? cmul(scale, make_double2(P.init_re, P.init_im)) : scale;
+      W::phase(r, C, F, sc, PRR);
+      W::template mix<31u>(r, P.tf[1][RPH], P.td[1][RPH]);
     }
     // back to L1 (conflict-free against the TMA layout) through the region
     __syncwarp();
@@ -336,7 +396,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
     __syncwarp();
 #pragma unroll
     for (int b = 0; b < 32; ++b) r[b] = rg[W::slot(lane, b)];
-    if constexpr (PH) W::template mix<31u>(r, P.tf[1][RPH + 1]);
+    if constexpr (PH) W::template mix<31u>(r, P.tf[1][RPH + 1], P.td[1][RPH + 1]);
     // every warp of the tile is past its region reads: write the tile back in
     // the TMA layout and store it with one bulk tensor copy; the storing
     // thread then refills the stage with the tile nst steps ahead
@@ -347,7 +407,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
     team_sync_n(1 + team, kWdWarps * 32);
     if (wq == kWdWarps - 1 && lane == 0) {  // warp 0 computes the next tile's fields
       const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
-      tma_store_5d(f.tmap, st, 0, 0, c1, 0, c4);
+      tma_store_5d(&P.tmap, st, 0, 0, c1, 0, c4);
       bulk_commit();
       bulk_wait_read<0>();
       feed(s, k + nst);

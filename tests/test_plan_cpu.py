@@ -147,8 +147,8 @@ def test_plan_structure(lib, n, pb):
             # global I/O layouts: lanes walk contiguous units (never the lo=0
             # layout of group A; H layouts keep register units above the run)
             if sw.get("prog") == 1:
-                # warp-decoupled high-group sweep: TMA in, complex64 only
-                assert g["kind"] != "A" and pair == 1 and sw["kind"] in "PMF"
+                # warp-decoupled high-group sweep (TMA in / out)
+                assert g["kind"] != "A" and sw["kind"] in "PMF" and (pair == 1 or g["kind"] == "H")
                 continue
             for lo in {sw["rounds"][-1][0], sw["rounds"][0][0]}:
                 if g["kind"] == "A":
