@@ -206,6 +206,13 @@ inline Plan make_plan(int n, int pair, int p) {
     seq.push_back(0);
     for (int i = 2; i < S - 1; ++i) seq.push_back(i);
     seq.push_back(S - 1);
+    // the last layer enters one end group through an F and mixes the other
+    // end with a plain M: let that M fall on the cheaper (H4: 128 B runs) end
+    {
+      const int first_last = (p == 1 || (p - 2) % 2 == 1) ? seq.front() : seq.back();
+      const int other = first_last == seq.front() ? seq.back() : seq.front();
+      if (P.groups[other].kind == GK_H && P.groups[first_last].kind == GK_H4) std::reverse(seq.begin(), seq.end());
+    }
     const char* nowd = getenv("LRQ_NO_WD");  // debugging: classic kernels, same order
     auto wd = [&](int gi, int kind) {
       // F only: a lone high-group M (last layer) streams faster on the classic TMA kernel
