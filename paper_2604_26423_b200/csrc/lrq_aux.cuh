@@ -187,6 +187,95 @@ __global__ void __launch_bounds__(1024) finalize_kernel(long long T, const doubl
   }
 }
 
+// Multi-CTA form of finalize_kernel for large tile counts (fixed order, so
+// still deterministic): pass 1 reduces block b's contiguous tile range and
+// writes the block-relative exclusive prefix; pass 2 combines the block
+// totals in order (out[], block offsets, prefix[T]); pass 3 adds the offsets.
+constexpr int kFinBlocks = 512;
+__global__ void __launch_bounds__(256) finalize_blocks(long long T, long long per_block, const double* __restrict__ rp,
+                                                       const double* __restrict__ rpe,
+                                                       const double* __restrict__ rmin,
+                                                       const unsigned long long* __restrict__ rarg,
+                                                       double* __restrict__ prefix, double* __restrict__ bs) {
+  __shared__ double s_p[256], s_pe[256], s_min[256];
+  __shared__ unsigned long long s_arg[256];
+  const int b = blockIdx.x, t = threadIdx.x;
+  const long long lo = min(T, (long long)b * per_block), hi = min(T, lo + per_block);
+  const long long per_t = (hi - lo + 255) / 256;
+  const long long tlo = min(hi, lo + per_t * t), thi = min(hi, tlo + per_t);
+  double a = 0.0, c = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  unsigned long long z = ~0ull;
+  for (long long i = tlo; i < thi; ++i) {
+    a += rp[i];
+    c += rpe[i];
+    if (rmin[i] < mn || (rmin[i] == mn && rarg[i] < z)) {
+      mn = rmin[i];
+      z = rarg[i];
+    }
+  }
+  s_p[t] = a;
+  s_pe[t] = c;
+  s_min[t] = mn;
+  s_arg[t] = z;
+  __syncthreads();
+  if (t == 0) {
+    double acc = 0.0, accb = 0.0, m = s_min[0];
+    unsigned long long zz = s_arg[0];
+    for (int i = 0; i < 256; ++i) {
+      const double x = s_p[i];
+      s_p[i] = acc;
+      acc += x;
+      accb += s_pe[i];
+      if (s_min[i] < m || (s_min[i] == m && s_arg[i] < zz)) {
+        m = s_min[i];
+        zz = s_arg[i];
+      }
+    }
+    bs[b] = acc;
+    bs[kFinBlocks + b] = accb;
+    bs[2 * kFinBlocks + b] = m;
+    bs[3 * kFinBlocks + b] = __longlong_as_double((long long)zz);
+  }
+  __syncthreads();
+  double run = s_p[t];
+  for (long long i = tlo; i < thi; ++i) {
+    prefix[i] = run;
+    run += rp[i];
+  }
+}
+
+__global__ void finalize_combine(int nb, long long T, double* __restrict__ bs, double* __restrict__ prefix,
+                                 double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0, accb = 0.0, m = bs[2 * kFinBlocks];
+  unsigned long long zz = (unsigned long long)__double_as_longlong(bs[3 * kFinBlocks]);
+  for (int i = 0; i < nb; ++i) {
+    const double x = bs[i];
+    bs[4 * kFinBlocks + i] = acc;  // exclusive block offset
+    acc += x;
+    accb += bs[kFinBlocks + i];
+    const double mi = bs[2 * kFinBlocks + i];
+    const unsigned long long zi = (unsigned long long)__double_as_longlong(bs[3 * kFinBlocks + i]);
+    if (mi < m || (mi == m && zi < zz)) {
+      m = mi;
+      zz = zi;
+    }
+  }
+  out[0] = acc;
+  out[1] = accb;
+  out[2] = m;
+  out[3] = __longlong_as_double((long long)zz);
+  prefix[T] = acc;
+}
+
+__global__ void __launch_bounds__(256) finalize_offsets(long long T, long long per_block, const double* __restrict__ bs,
+                                                        double* __restrict__ prefix) {
+  const int b = blockIdx.x;
+  const long long lo = min(T, (long long)b * per_block), hi = min(T, lo + per_block);
+  const double off = bs[4 * kFinBlocks + b];
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) prefix[i] += off;
+}
+
 // ---------------------------------------------------------------------------
 // Two-level inverse-CDF sampler (reference engine.py:254-263: first index
 // whose normalised cumulative probability exceeds u).  One warp per shot:

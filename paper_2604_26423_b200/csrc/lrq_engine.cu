@@ -147,6 +147,7 @@ struct lrq_state {
   double* red = nullptr;     // 4 arrays of num_tiles (p, pE, minE, arg bits)
   double* prefix = nullptr;  // num_tiles + 1
   double* out = nullptr;     // 4 finalize scalars
+  double* fin = nullptr;     // 5 * kFinBlocks finalize scratch
   double* dW = nullptr;      // n*n cost matrix
   double* dzero = nullptr;   // n zeros (no global qubits on a single device)
   double* dJ = nullptr;      // p*n*n phase matrices
@@ -188,6 +189,7 @@ void free_state(lrq_state* s) {
   cudaFree(s->red);
   cudaFree(s->prefix);
   cudaFree(s->out);
+  cudaFree(s->fin);
   cudaFree(s->dW);
   cudaFree(s->dzero);
   cudaFree(s->dJ);
@@ -459,6 +461,29 @@ int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int gri
   return launch_sweep_kind<double>(s->stream, gk, sk, sp_in, grid, smem);
 }
 
+// deterministic combine of the per-tile partials + CDF prefix (lrq_aux.cuh);
+// bs: 5 * kFinBlocks doubles of scratch (multi-CTA path for large T)
+int launch_finalize(cudaStream_t st, long long T, double* red, double* prefix, double* out, double* bs) {
+  double* rp = red;
+  double* rpe = red + T;
+  double* rmin = red + 2 * T;
+  unsigned long long* rarg = reinterpret_cast<unsigned long long*>(red + 3 * T);
+  if (T < 8192 || !bs) {
+    finalize_kernel<<<1, 1024, 0, st>>>(T, rp, rpe, rmin, rarg, prefix, out);
+    CUDA_TRY(cudaGetLastError());
+    return LRQ_OK;
+  }
+  const long long per = (T + kFinBlocks - 1) / kFinBlocks;
+  const int nb = (int)((T + per - 1) / per);
+  finalize_blocks<<<nb, 256, 0, st>>>(T, per, rp, rpe, rmin, rarg, prefix, bs);
+  CUDA_TRY(cudaGetLastError());
+  finalize_combine<<<1, 32, 0, st>>>(nb, T, bs, prefix, out);
+  CUDA_TRY(cudaGetLastError());
+  finalize_offsets<<<nb, 256, 0, st>>>(T, per, bs, prefix);
+  CUDA_TRY(cudaGetLastError());
+  return LRQ_OK;
+}
+
 template <typename T>
 int launch_small(const SmallParams& sp, size_t smem, cudaStream_t st) {
   static std::once_flag once;
@@ -715,8 +740,10 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
       record(s, ev++, 'T');
     }
   }
-  finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
-  CUDA_TRY(cudaGetLastError());
+  {
+    const int rc = launch_finalize(s->stream, s->num_tiles, s->red, s->prefix, s->out, s->fin);
+    if (rc) return rc;
+  }
   record(s, ev++, 'Z');
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   if (s->timing) {
@@ -866,6 +893,7 @@ int lrq_create(int n, int pbytes, int device, uint64_t budget, lrq_state** out) 
   if (e == cudaSuccess) e = cudaMalloc(&s->red, sizeof(double) * 4 * s->num_tiles);
   if (e == cudaSuccess) e = cudaMalloc(&s->prefix, sizeof(double) * (s->num_tiles + 1));
   if (e == cudaSuccess) e = cudaMalloc(&s->out, sizeof(double) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->fin, sizeof(double) * 5 * kFinBlocks);
   // zero-fills on the engine's own (non-blocking) stream and waited for: a
   // legacy-stream cudaMemset is not ordered with it and could land after the
   // first lrq_set_cost copy
@@ -1185,8 +1213,10 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       record(s, ev++, 'X');
     }
   }
-  finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
-  CUDA_TRY(cudaGetLastError());
+  {
+    const int rc = launch_finalize(s->stream, s->num_tiles, s->red, s->prefix, s->out, s->fin);
+    if (rc) return rc;
+  }
   record(s, ev++, 'Z');
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   if (s->timing) {
@@ -1272,8 +1302,10 @@ int lrq_recompute(lrq_state* s) {
     int rc = launch_sweep(s, GK_A, SK_Q, sp, (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap));
     if (rc) return rc;
   }
-  finalize_kernel<<<1, 1024, 0, s->stream>>>(s->num_tiles, rp, rpe, rmin, rarg, s->prefix, s->out);
-  CUDA_TRY(cudaGetLastError());
+  {
+    const int rc = launch_finalize(s->stream, s->num_tiles, s->red, s->prefix, s->out, s->fin);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->reduced = true;
   s->rank_sum_p.clear();
@@ -1473,7 +1505,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
     // exhaustive E_w scan over z with top bit 0 (complement symmetry), NOAMPS sweep
     const long long tiles = 1ll << (n - K - 1 >= 0 ? n - K - 1 : 0);
     const long long T = (n - 1 >= K) ? tiles : 1;
-    double *dW = nullptr, *red = nullptr, *prefix = nullptr, *out = nullptr, *zero = nullptr;
+    double *dW = nullptr, *red = nullptr, *prefix = nullptr, *out = nullptr, *zero = nullptr, *fin = nullptr;
     cudaStream_t st;
     CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     std::vector<double> M((size_t)n * n);
@@ -1483,6 +1515,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
     if (e == cudaSuccess) e = cudaMalloc(&prefix, sizeof(double) * (T + 1));
     if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(double) * 4);
     if (e == cudaSuccess) e = cudaMalloc(&zero, sizeof(double) * (n + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&fin, sizeof(double) * 5 * kFinBlocks);
     if (e == cudaSuccess) e = cudaMemsetAsync(zero, 0, sizeof(double) * (n + 1), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(red, 0, sizeof(double) * 2 * T, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dW, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, st);
@@ -1509,9 +1542,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
       if (launch_sweep_t<float, GK_A, SK_N>(st, sp, grid, smem) != LRQ_OK) e = cudaErrorUnknown;
     }
     if (e == cudaSuccess) {
-      finalize_kernel<<<1, 1024, 0, st>>>(T, red, red + T, red + 2 * T,
-                                          reinterpret_cast<unsigned long long*>(red + 3 * T), prefix, out);
-      e = cudaGetLastError();
+      if (launch_finalize(st, T, red, prefix, out, fin) != LRQ_OK) e = cudaErrorUnknown;
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(&best, out + 3, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -1520,6 +1551,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
     cudaFree(prefix);
     cudaFree(out);
     cudaFree(zero);
+    cudaFree(fin);
     cudaStreamDestroy(st);
     CUDA_TRY(e);
   }
