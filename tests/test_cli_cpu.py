@@ -1,0 +1,29 @@
+"""CPU tests of the gen/simulate command line (host-side parts only)."""
+import json
+import os
+
+import pytest
+
+from paper_2604_26423_b200.cli import main
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_gen_without_solve_matches_reference_instance(tmp_path):
+    out = tmp_path / "i.json"
+    assert main(["gen", "--n", "12", "--seed", "7", "--out", str(out), "--solve-limit", "0"]) == 0
+    got = json.loads(out.read_text())
+    want = json.load(open(os.path.join(GOLDEN, "cli_n12_inst.json")))
+    assert got["n"] == want["n"] and got["edges"] == want["edges"]  # same Philox weights, bit for bit
+    assert got["optimal"] is None
+    man = json.loads((tmp_path / "i.json.manifest.json").read_text())
+    assert man["command"] == "gen" and str(out) in man["outputs"]
+
+
+def test_simulate_input_errors_exit_2(tmp_path, capsys):
+    assert main(["simulate", "--instance", str(tmp_path / "missing.json"), "--out", str(tmp_path / "r.json")]) == 2
+    inst = os.path.join(GOLDEN, "cli_n12_inst.json")
+    assert main(["simulate", "--instance", inst, "--out", str(tmp_path / "r.json"), "--mode", "noisy"]) == 2
+    assert "noiseless mode only" in capsys.readouterr().err
+    with pytest.raises(SystemExit):
+        main(["simulate", "--instance", inst, "--out", str(tmp_path / "r.json"), "--precision", "fp16"])
