@@ -731,7 +731,7 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
-    int rc = launch_sweep(s, gr.kind, w.kind, sp, grid);
+    int rc = w.prog == 1 ? launch_wd(s, gr.kind, w.kind, sp) : launch_sweep(s, gr.kind, w.kind, sp, grid);
     if (rc) return rc;
     record(s, ev++, "PMFRLQN"[w.kind]);
     if (w.remap_after) {

@@ -321,6 +321,10 @@ inline Plan make_dist_plan(int n_loc, int g, int pair, int p) {
   PlanSweep q = make_sweep(0, SK_Q, -1, -1, -1, true);
   q.perm = 0;
   P.sweeps.push_back(q);
+  // P and F sweeps of the (high) group Z run the warp-decoupled kernel
+  const char* nowd = getenv("LRQ_NO_WD");
+  for (PlanSweep& s : P.sweeps)
+    if (!(nowd && *nowd == '1') && P.groups[s.group].kind != GK_A && (s.kind == SK_P || s.kind == SK_F)) s.prog = 1;
   for (PlanSweep& s : P.sweeps) plan_rounds(P.groups[s.group], pair, s);
   return P;
 }

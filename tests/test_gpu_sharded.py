@@ -124,3 +124,21 @@ def test_scaling_sweeps():
     recs = L.scaling_sweep(L.SweepConfig(mode="size", nq_values=(16, 17, 18), nq_local=15, p=2, precision="fp64"))
     vols = [r.amps_exchanged for r in recs]
     assert vols == sorted(vols) and vols[0] < vols[-1]
+
+
+@pytest.mark.parametrize("n,G,p,prec,dbeta", [(26, 2, 3, "fp32", 1.2), (24, 4, 2, "fp64", 0.2), (26, 8, 3, "fp64", 0.9)])
+def test_larger_sharded_runs_match_dense(n, G, p, prec, dbeta):
+    """Three-group local plans: the shards' P/F sweeps on Z run the
+    warp-decoupled kernel with rank-local fields; checked against the dense
+    engine (itself checked against the oracle)."""
+    inst = L.generate_instance(n, 4)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=p, delta_beta=dbeta))
+    sv, rec = L.run_circuit_sharded(circ, L.plan_for_shard_count(n, G), prec)
+    try:
+        assert isinstance(sv, L.ShardedStateVector)
+        dense = L.run_circuit(circ, prec)
+        tol = 1e-12 if prec == "fp64" else 3e-6
+        assert normwise(sv.amps, dense.amps.astype(np.complex128)) < tol
+        dense.release()
+    finally:
+        sv.release()
