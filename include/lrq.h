@@ -77,6 +77,19 @@ int lrq_run(lrq_state *s, int p, const double *phase, const double *mixer);
 int lrq_run_fields(lrq_state *s, int p, const double *phase, const double *field, const double *constant,
                    const double *mixer);
 
+/* Noisy Monte Carlo trajectories (noise.py:109-207) for small n (n below the
+ * tile: 12 complex128 / 13 complex64), batched one trajectory per CTA.
+ * Trajectory t is the ideal circuit with its Pauli insertions propagated to
+ * the end: per-layer edge angles phase[(t*p + k)*E + e] (signs flipped by X/Y
+ * insertions), per-qubit mixer half-angles mixer[(t*p + k)*n + q] (equal up
+ * to sign within a layer; Z/Y flip the sign), and a final X mask xmask[t]
+ * (probabilities permuted z -> z ^ mask).  Writes trajectory probabilities
+ * (float64, T x 2^n, may be NULL) and, if shots > 0, inverse-CDF draws with
+ * the caller's uniforms u[t*shots + i] into idx_out[t*shots + i].          */
+int lrq_noisy_batch(int num_qubits, int precision_bytes, int device, int trajectories, int p, const double *phase,
+                    const double *mixer, const unsigned *xmask, int64_t shots, const double *u, double *probs_out,
+                    uint64_t *idx_out);
+
 /* reductions of the last run (exact_expected_r numerator, engine.py:214-226;
  * exhaustive max cut argmax, problem.py:174-211).                            */
 int lrq_reduce(lrq_state *s, lrq_reduction *out);

@@ -25,6 +25,7 @@ from .engine import (
     StateVector,
     check_memory,
     exact_expected_r,
+    expected_r_from_probs,
     run_circuit,
     sample,
     save_statevector,
@@ -67,4 +68,15 @@ from .sharded import (
     run_circuit_sharded,
     scaling_sweep,
     write_timing_csv,
+)
+from .noise import (
+    DepolarizingConfig,
+    NoiseFit,
+    epsilon_accumulated,
+    fit_k0,
+    noisy_expected_probs,
+    noisy_expected_r,
+    predict_r_overlap,
+    r_overlap,
+    run_noisy_ensemble,
 )

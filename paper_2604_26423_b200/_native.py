@@ -42,6 +42,7 @@ _SIGNATURES = {
     "lrq_set_cost": ([_state_p, _p], _c_int),
     "lrq_run": ([_state_p, _c_int, _p, _p], _c_int),
     "lrq_run_fields": ([_state_p, _c_int, _p, _p, _p, _p], _c_int),
+    "lrq_noisy_batch": ([_c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _c_i64, _p, _p, _p], _c_int),
     "lrq_reduce": ([_state_p, ctypes.POINTER(Reduction)], _c_int),
     "lrq_recompute": ([_state_p], _c_int),
     "lrq_sample": ([_state_p, _p, _c_i64, _p], _c_int),
@@ -354,3 +355,26 @@ def max_cut(n: int, w: np.ndarray, device: int | None = None):
     v = _c_dbl(0.0)
     check(lib().lrq_max_cut(n, ptr(w), dev, ctypes.byref(z), ctypes.byref(v)))
     return int(z.value), float(v.value)
+
+
+def noisy_batch(n: int, precision_bytes: int, phase: np.ndarray, mixer: np.ndarray, xmask: np.ndarray,
+                u: np.ndarray | None = None, want_probs: bool = True, device: int | None = None):
+    """Batched small-n trajectories (lrq_noisy_batch): phase (T, p, E), mixer
+    (T, p, n), xmask (T,), u (T, S) or None -> (probs (T, 2^n) | None,
+    indices (T, S) | None)."""
+    phase = np.ascontiguousarray(phase, dtype=np.float64)
+    mixer = np.ascontiguousarray(mixer, dtype=np.float64)
+    xmask = np.ascontiguousarray(xmask, dtype=np.uint32)
+    T, p = mixer.shape[0], mixer.shape[1]
+    dev = default_device() if device is None else int(device)
+    probs = np.empty((T, 1 << n), dtype=np.float64) if want_probs else None
+    shots = 0 if u is None else int(u.shape[1])
+    idx = None
+    if shots:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        idx = np.empty((T, shots), dtype=np.uint64)
+    check(lib().lrq_noisy_batch(n, precision_bytes, dev, T, p, ptr(phase), ptr(mixer), ptr(xmask), shots,
+                                ptr(u) if shots else None, ptr(probs) if probs is not None else None,
+                                ptr(idx) if idx is not None else None))
+    return probs, idx
+

@@ -18,6 +18,14 @@ struct SmallParams {
   const double* W;    // n * n cost matrix (may be null: no reduction)
   const double* F;    // p * n single-Z fields (may be null)
   const double* Fc;   // p constant phases (with F)
+  // batched noisy trajectories (lrq_noisy_batch): block b runs trajectory b
+  // with its own J (b * strideJ), per-qubit mixer signs msign[b*p*n + k*n + q]
+  // (sin h -> -sin h where negative; null: all +), and writes the trajectory's
+  // probabilities, index-permuted by its Pauli X mask, to probs[b * 2^n + ...]
+  const signed char* msign;
+  long long strideJ;
+  const unsigned* xmask;
+  double* probs;
   double init_re, init_im;
   int load;  // start from the stored state instead of the init value
   int min_bit;
@@ -35,6 +43,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   V* s = reinterpret_cast<V*>(smem);
   double* red = reinterpret_cast<double*>(s + N);  // 8 warps * 4
   const int t = threadIdx.x;
+  const int b = blockIdx.x;  // trajectory (batch); 0 for a single state
   const V* g0 = reinterpret_cast<const V*>(P.amps);
   for (int z = t; z < N; z += blockDim.x) {
     if (P.load) {
@@ -45,8 +54,9 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
     }
   }
   __syncthreads();
+  const signed char* msign = P.msign ? P.msign + (size_t)b * P.p * n : nullptr;
   for (int k = 0; k < P.p; ++k) {
-    const double* J = P.J + (size_t)k * n * n;
+    const double* J = P.J + (size_t)b * P.strideJ + (size_t)k * n * n;
     for (int z = t; z < N; z += blockDim.x) {
       double e = 0.0;
       for (int i = 0; i < n; ++i)
@@ -58,8 +68,9 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
       s[z] = cmul_amp(s[z], expmi(e));
     }
     __syncthreads();
-    const T c = (T)P.mix[2 * k], sn = (T)P.mix[2 * k + 1];
+    const T c = (T)P.mix[2 * k], sn0 = (T)P.mix[2 * k + 1];
     for (int q = 0; q < n; ++q) {
+      const T sn = (msign && msign[k * n + q] < 0) ? -sn0 : sn0;
       for (int pi = t; pi < N / 2; pi += blockDim.x) {
         const int lo = ((pi >> q) << (q + 1)) | (pi & ((1 << q) - 1));
         const int hi = lo | (1 << q);
@@ -74,6 +85,12 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
       }
       __syncthreads();
     }
+  }
+  if (P.probs) {
+    const unsigned m = P.xmask ? P.xmask[b] : 0u;
+    double* out = P.probs + (size_t)b * N;
+    for (int z = t; z < N; z += blockDim.x) out[z ^ m] = prob(s[z]);
+    return;
   }
   V* g = reinterpret_cast<V*>(P.amps);
   for (int z = t; z < N; z += blockDim.x) g[z] = s[z];
@@ -274,6 +291,36 @@ __global__ void __launch_bounds__(256) finalize_offsets(long long T, long long p
   const long long lo = min(T, (long long)b * per_block), hi = min(T, lo + per_block);
   const double off = bs[4 * kFinBlocks + b];
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) prefix[i] += off;
+}
+
+// Inverse-CDF draws for a batch of small distributions (noisy trajectories):
+// block b owns probs[b * N ...]; cdf = sequential cumsum, normalised by its
+// last element, first index with cdf > u (reference engine.py:254-263).
+__global__ void __launch_bounds__(256) batch_sample_kernel(const double* __restrict__ probs, int N,
+                                                           const double* __restrict__ u, long long S,
+                                                           unsigned long long* __restrict__ out) {
+  extern __shared__ double cdf[];
+  const int b = blockIdx.x;
+  const double* pr = probs + (size_t)b * N;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < N; ++i) {
+      acc += pr[i];
+      cdf[i] = acc;
+    }
+  }
+  __syncthreads();
+  const double total = cdf[N - 1];
+  for (long long k = threadIdx.x; k < S; k += blockDim.x) {
+    const double x = u[(size_t)b * S + k];
+    int lo = 0, hi = N;  // first i in [0, N) with cdf[i] / total > x (N if none)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cdf[mid] / total > x) hi = mid;
+      else lo = mid + 1;
+    }
+    out[(size_t)b * S + k] = (unsigned long long)(lo < N ? lo : N - 1);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -485,14 +485,14 @@ int launch_finalize(cudaStream_t st, long long T, double* red, double* prefix, d
 }
 
 template <typename T>
-int launch_small(const SmallParams& sp, size_t smem, cudaStream_t st) {
+int launch_small(const SmallParams& sp, size_t smem, cudaStream_t st, int grid = 1) {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
     err = cudaFuncSetAttribute(small_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   });
   CUDA_TRY(err);
-  small_kernel<T><<<1, 256, smem, st>>>(sp);
+  small_kernel<T><<<grid, 256, smem, st>>>(sp);
   CUDA_TRY(cudaGetLastError());
   return LRQ_OK;
 }
@@ -1135,6 +1135,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
 
   if (n < s->K) {
     SmallParams sp;
+    memset(&sp, 0, sizeof sp);
     sp.amps = s->amps;
     sp.n = n;
     sp.p = p;
@@ -1249,6 +1250,103 @@ int lrq_run_fields(lrq_state* s, int p, const double* phase, const double* field
   s->field_h.clear();
   s->cst_h.clear();
   return rc;
+}
+
+int lrq_noisy_batch(int n, int pbytes, int device, int trajectories, int p, const double* phase,
+                    const double* mixer, const unsigned* xmask, int64_t shots, const double* u, double* probs_out,
+                    uint64_t* idx_out) {
+  if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
+  const int K = tile_amp_bits(pbytes);
+  if (n < 1 || n >= K)
+    return fail(LRQ_EVALIDATION, "batched trajectories need 1 <= n < " + std::to_string(K) + " (use lrq_run_ex above)");
+  if (trajectories < 1 || p < 1) return fail(LRQ_EVALIDATION, "need at least one trajectory and one layer");
+  if (!phase || !mixer || (shots > 0 && (!u || !idx_out))) return fail(LRQ_EVALIDATION, "null argument");
+  const int E = n * (n - 1) / 2, N = 1 << n;
+  // per layer the mixer half-angles may differ only in sign across qubits and trajectories
+  std::vector<double> mix(2 * (size_t)p);
+  std::vector<signed char> sg((size_t)trajectories * p * n);
+  for (int k = 0; k < p; ++k) {
+    const double h0 = fabs(mixer[(size_t)k * n]);
+    mix[2 * k] = cos(h0);
+    mix[2 * k + 1] = -sin(h0);
+    for (int t = 0; t < trajectories; ++t)
+      for (int q = 0; q < n; ++q) {
+        const double h = mixer[((size_t)t * p + k) * n + q];
+        if (!isfinite(h) || fabs(h) != h0)
+          return fail(LRQ_EVALIDATION, "per-qubit mixer angles of a layer must agree up to sign");
+        sg[((size_t)t * p + k) * n + q] = h < 0 ? -1 : 1;
+      }
+  }
+  std::vector<double> J((size_t)trajectories * p * n * n);
+  for (long long i = 0; i < (long long)trajectories * p; ++i) {
+    for (int e = 0; e < E; ++e)
+      if (!isfinite(phase[i * E + e])) return fail(LRQ_EVALIDATION, "phase angle is not finite");
+    sym_matrix(n, phase + i * E, J.data() + (size_t)i * n * n);
+  }
+  DeviceGuard guard(device);
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double *dJ = nullptr, *dmix = nullptr, *dprobs = nullptr, *du = nullptr;
+  signed char* dsg = nullptr;
+  unsigned* dmask = nullptr;
+  unsigned long long* didx = nullptr;
+  cudaError_t e = cudaMalloc(&dJ, sizeof(double) * J.size());
+  if (e == cudaSuccess) e = cudaMalloc(&dmix, sizeof(double) * mix.size());
+  if (e == cudaSuccess) e = cudaMalloc(&dsg, sg.size());
+  if (e == cudaSuccess) e = cudaMalloc(&dmask, sizeof(unsigned) * trajectories);
+  if (e == cudaSuccess) e = cudaMalloc(&dprobs, sizeof(double) * (size_t)trajectories * N);
+  if (e == cudaSuccess && shots > 0) e = cudaMalloc(&du, sizeof(double) * (size_t)trajectories * shots);
+  if (e == cudaSuccess && shots > 0) e = cudaMalloc(&didx, sizeof(unsigned long long) * (size_t)trajectories * shots);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dJ, J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dmix, mix.data(), sizeof(double) * mix.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dsg, sg.data(), sg.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    if (xmask) e = cudaMemcpyAsync(dmask, xmask, sizeof(unsigned) * trajectories, cudaMemcpyHostToDevice, st);
+    else e = cudaMemsetAsync(dmask, 0, sizeof(unsigned) * trajectories, st);
+  }
+  if (e == cudaSuccess && shots > 0)
+    e = cudaMemcpyAsync(du, u, sizeof(double) * (size_t)trajectories * shots, cudaMemcpyHostToDevice, st);
+  int rc = LRQ_OK;
+  if (e == cudaSuccess) {
+    SmallParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.n = n;
+    sp.p = p;
+    sp.J = dJ;
+    sp.strideJ = (long long)p * n * n;
+    sp.mix = dmix;
+    sp.msign = dsg;
+    sp.xmask = dmask;
+    sp.probs = dprobs;
+    sp.init_re = pbytes == 8 ? init_amplitude<float>(n) : init_amplitude<double>(n);
+    sp.min_bit = -2;
+    const size_t smem = (size_t)pbytes * N + 8 * 4 * 8;
+    if (pbytes == 8) {
+      rc = launch_small<float>(sp, smem, st, trajectories);
+    } else {
+      rc = launch_small<double>(sp, smem, st, trajectories);
+    }
+    if (!rc && shots > 0) {
+      batch_sample_kernel<<<trajectories, 256, sizeof(double) * N, st>>>(dprobs, N, du, shots, didx);
+      e = cudaGetLastError();
+    }
+  }
+  if (!rc && e == cudaSuccess && probs_out)
+    e = cudaMemcpyAsync(probs_out, dprobs, sizeof(double) * (size_t)trajectories * N, cudaMemcpyDeviceToHost, st);
+  if (!rc && e == cudaSuccess && shots > 0)
+    e = cudaMemcpyAsync(idx_out, didx, sizeof(uint64_t) * (size_t)trajectories * shots, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(dJ);
+  cudaFree(dmix);
+  cudaFree(dsg);
+  cudaFree(dmask);
+  cudaFree(dprobs);
+  cudaFree(du);
+  cudaFree(didx);
+  cudaStreamDestroy(st);
+  if (rc) return rc;
+  CUDA_TRY(e);
+  return LRQ_OK;
 }
 
 int lrq_recompute(lrq_state* s) {

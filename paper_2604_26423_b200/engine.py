@@ -169,6 +169,26 @@ def run_circuit(circuit: CircuitIR, precision: Precision | str = Precision.FP32,
 # observables and sampling
 
 
+_EXPECTATION_CHUNK = 1 << 16
+
+
+def expected_r_from_probs(probs: np.ndarray, inst: WmcInstance) -> float:
+    """Expected approximation ratio of an explicit basis-state distribution
+    (engine.py:214-226): chunked probs . C / C*, cut values from the GPU."""
+    from .problem import cut_values_range
+
+    probs = np.asarray(probs, dtype=np.float64)
+    if probs.size != 1 << inst.num_vertices:
+        raise ValidationError(f"distribution over {probs.size} states does not match n={inst.num_vertices}")
+    if inst.optimal_cut is None:
+        raise StateError("instance has no optimal cut; solve it first")
+    total = 0.0
+    for lo in range(0, probs.size, _EXPECTATION_CHUNK):
+        hi = min(lo + _EXPECTATION_CHUNK, probs.size)
+        total += float(probs[lo:hi] @ cut_values_range(inst, lo, hi))
+    return total / inst.optimal_cut.value
+
+
 def exact_expected_r(sv: StateVector, inst: WmcInstance) -> float:
     """sum_z |a_z|^2 C(z) / C* over the full distribution (no sampling)."""
     if inst.num_vertices != sv.num_qubits:
