@@ -118,13 +118,54 @@ def trajectory_program(circuit: CircuitIR, cfg: DepolarizingConfig, trajectory: 
     return phase, mixer, mask
 
 
+def batch_programs(circuit: CircuitIR, cfg: DepolarizingConfig):
+    """trajectory_program for every trajectory at once: the Pauli frames of
+    all trajectories advance together through the gate list (numpy over the
+    trajectory axis).  Returns phase (T, p, E), mixer (T, p, n), xmask (T,)."""
+    n, T = circuit.num_qubits, cfg.trajectories
+    layers = _layers(circuit)
+    index = {pair: e for e, pair in enumerate(complete_edge_pairs(n))}
+    n_rzz = sum(len(rzz) for rzz, _ in layers)
+    phase = np.zeros((T, len(layers), len(index)))
+    mixer = np.zeros((T, len(layers), n))
+    if cfg.epsilon > 0.0:
+        fire = np.empty((T, n_rzz), dtype=bool)
+        codes = np.empty((T, n_rzz), dtype=np.int64)
+        for t in range(T):
+            rng = derive_rng(cfg.rng_seed, "trajectory", t)
+            fire[t] = rng.random(n_rzz) < _PAULI_BRANCH * cfg.epsilon
+            codes[t] = rng.integers(1, 16, size=n_rzz)
+        # X part / Z part of each code's Pauli on the gate's first / second qubit
+        pa, pb = np.divmod(np.where(fire, codes, 0), 4)
+        xa, za = (pa == 1) | (pa == 2), (pa == 2) | (pa == 3)
+        xb, zb = (pb == 1) | (pb == 2), (pb == 2) | (pb == 3)
+    x = np.zeros((T, n), dtype=bool)
+    z = np.zeros((T, n), dtype=bool)
+    k = 0
+    for li, (rzz, rx) in enumerate(layers):
+        for g in rzz:
+            a, b = g.qubits
+            e = index[(min(a, b), max(a, b))]
+            half = 0.5 * g.theta
+            phase[:, li, e] += np.where(x[:, a] ^ x[:, b], -half, half)
+            if cfg.epsilon > 0.0:
+                x[:, a] ^= xa[:, k]
+                z[:, a] ^= za[:, k]
+                x[:, b] ^= xb[:, k]
+                z[:, b] ^= zb[:, k]
+            k += 1
+        for g in rx:
+            q = g.qubits[0]
+            half = 0.5 * g.theta
+            mixer[:, li, q] = np.where(z[:, q], -half, half)
+    xmask = (x.astype(np.uint64) << np.arange(n, dtype=np.uint64)[None, :]).sum(axis=1).astype(np.uint32)
+    return phase, mixer, xmask
+
+
 def _batch(circuit: CircuitIR, cfg: DepolarizingConfig, precision: Precision, memory_budget, shots: int):
     n = circuit.num_qubits
     check_memory(n, precision, memory_budget)
-    progs = [trajectory_program(circuit, cfg, t) for t in range(cfg.trajectories)]
-    phase = np.stack([pr[0] for pr in progs])
-    mixer = np.stack([pr[1] for pr in progs])
-    xmask = np.array([pr[2] for pr in progs], dtype=np.uint32)
+    phase, mixer, xmask = batch_programs(circuit, cfg)
     u = None
     if shots:
         u = np.stack([derive_rng(cfg.rng_seed, "shots", t).random(shots) for t in range(cfg.trajectories)])

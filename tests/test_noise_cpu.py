@@ -116,3 +116,15 @@ def test_config_fit_and_overlap_arithmetic():
         L.fit_k0([(1.0, -0.2)])
     assert L.r_overlap(0.8, 0.6, 1.0) == pytest.approx(0.5)
     assert L.predict_r_overlap(0.5, 10, 0.1) == pytest.approx(2.0 ** -0.5)
+
+
+def test_batched_programs_equal_per_trajectory_programs():
+    from paper_2604_26423_b200.noise import batch_programs
+    circ = L.build_circuit(L.generate_instance(7, 3), L.LrQaoaParams(p=4))
+    cfg = L.DepolarizingConfig(0.15, trajectories=9, rng_seed=21)
+    ph, mx, mk = batch_programs(circ, cfg)
+    for t in range(cfg.trajectories):
+        p1, m1, k1 = trajectory_program(circ, cfg, t)
+        np.testing.assert_array_equal(ph[t], p1)
+        np.testing.assert_array_equal(mx[t], m1)
+        assert int(mk[t]) == k1
