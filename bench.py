@@ -166,6 +166,15 @@ def profiled_traffic():
 # CPU reference arm: the oracle port of the reference per-gate engine
 
 
+def kernel_launches(kinds, n_local, tile_bits=13):
+    """Kernel launches behind the engine's timing records: one per sweep
+    ('P','M','F','R','Q'), three for the multi-CTA finalize ('Z', tile count
+    >= 8192), two for a deferred-flip reversal ('X'), one per remap chunk
+    group is counted as one ('T')."""
+    z = 3 if (1 << max(0, n_local - tile_bits)) >= 8192 else 1
+    return sum(z if k == "Z" else 2 if k == "X" else 1 for k in kinds)
+
+
 def cpu_reference(n, p, precision, budget_s, seed):
     """Time the reference's per-gate numpy kernels (oracle port, all host cores)
     on a bounded sample of the workload and extrapolate to one layer:
@@ -295,7 +304,7 @@ def run_ours(args, rank, world, local_rank, dist):
     per_launch_achieved = alg / sweep_time_s / 1e9
     peak, peak_kind = measured_peak()
     traffic = profiled_traffic()
-    launches_per_step = len(sweep_ms) // args.steps + 1  # + sample kernel
+    launches_per_step = kernel_launches(kinds_all, n) // args.steps + 1  # + sample kernel
     amp_updates = float(1 << n) * p * args.steps * world
     E = n * (n - 1) // 2
     h2d = lay.phase.nbytes + lay.mixer.nbytes + w.nbytes + args.shots * 8
@@ -426,7 +435,7 @@ def run_ours_dist(args, rank, world, local_rank, dist):
     peak, peak_kind = measured_peak()
     amp_updates = float(1 << n) * p * args.steps
     E = n * (n - 1) // 2
-    launches_per_step = len(ms_all) // args.steps + 1
+    launches_per_step = kernel_launches(kinds_all, nl) // args.steps + 1  # + sample kernel
     return {
         "metric": METRIC,
         "value": amp_updates / (dev_ms_max * 1e-3),
