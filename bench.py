@@ -167,12 +167,12 @@ def profiled_traffic():
 
 
 def kernel_launches(kinds, n_local, tile_bits=13):
-    """Kernel launches behind the engine's timing records: one per sweep
+    """Our kernel launches behind the engine's timing records: one per sweep
     ('P','M','F','R','Q'), three for the multi-CTA finalize ('Z', tile count
-    >= 8192), two for a deferred-flip reversal ('X'), one per remap chunk
-    group is counted as one ('T')."""
+    >= 8192), two for a deferred-flip reversal ('X'); remaps ('T') are NCCL
+    send/recv plus copies, not our kernels."""
     z = 3 if (1 << max(0, n_local - tile_bits)) >= 8192 else 1
-    return sum(z if k == "Z" else 2 if k == "X" else 1 for k in kinds)
+    return sum(z if k == "Z" else 2 if k == "X" else 0 if k == "T" else 1 for k in kinds)
 
 
 def cpu_reference(n, p, precision, budget_s, seed):
