@@ -77,6 +77,14 @@ int lrq_run(lrq_state *s, int p, const double *phase, const double *mixer);
 int lrq_run_fields(lrq_state *s, int p, const double *phase, const double *field, const double *constant,
                    const double *mixer);
 
+/* Gate-by-gate execution (engine.py:99-195) for circuits of any other shape:
+ * reset to |0...0> (which = 0) or to the uniform state 2^(-n/2) (which = 1,
+ * init_plus_state), then apply H (kind 0), RX(theta) (1) or RZZ(theta) (2)
+ * one full pass at a time, with the reference kernels' complex arithmetic.
+ * Asynchronous on the engine stream; lrq_recompute / lrq_sample after.     */
+int lrq_reset(lrq_state *s, int which);
+int lrq_apply_gate(lrq_state *s, int kind, int q0, int q1, double theta);
+
 /* Noisy Monte Carlo trajectories (noise.py:109-207) for small n (n below the
  * tile: 12 complex128 / 13 complex64), batched one trajectory per CTA.
  * Trajectory t is the ideal circuit with its Pauli insertions propagated to

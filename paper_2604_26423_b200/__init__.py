@@ -21,6 +21,12 @@ from .circuit import (
 )
 from .engine import (
     Precision,
+    apply_gate,
+    apply_h,
+    apply_rx,
+    apply_rzz,
+    init_plus_state,
+    zero_state,
     ShotSet,
     StateVector,
     check_memory,

@@ -42,6 +42,8 @@ _SIGNATURES = {
     "lrq_set_cost": ([_state_p, _p], _c_int),
     "lrq_run": ([_state_p, _c_int, _p, _p], _c_int),
     "lrq_run_fields": ([_state_p, _c_int, _p, _p, _p, _p], _c_int),
+    "lrq_reset": ([_state_p, _c_int], _c_int),
+    "lrq_apply_gate": ([_state_p, _c_int, _c_int, _c_int, _c_dbl], _c_int),
     "lrq_noisy_batch": ([_c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _c_i64, _p, _p, _p], _c_int),
     "lrq_reduce": ([_state_p, ctypes.POINTER(Reduction)], _c_int),
     "lrq_recompute": ([_state_p], _c_int),
@@ -260,6 +262,12 @@ class DeviceState:
         if field.size != p * self.n or constant.size != p:
             raise ValidationError(f"fields need shape ({p}, {self.n}) and constants ({p},)")
         check(lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
+
+    def reset(self, which: int = 0) -> None:
+        check(lib().lrq_reset(self.handle, int(which)))
+
+    def apply_gate(self, kind: int, q0: int, q1: int = 0, theta: float = 0.0) -> None:
+        check(lib().lrq_apply_gate(self.handle, int(kind), int(q0), int(q1), float(theta)))
 
     def reduce(self) -> Reduction:
         r = Reduction()

@@ -293,6 +293,81 @@ __global__ void __launch_bounds__(256) finalize_offsets(long long T, long long p
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) prefix[i] += off;
 }
 
+// Gate-by-gate kernels (reference engine.py:128-166, for circuits that are
+// not H + p x (RZZ, RX^n)): one pass over the state per gate, with the
+// reference's complex arithmetic (products and sums rounded one by one, no
+// FMA contraction).  kind 0: H, 1: RX(theta).
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T>
+__global__ void gate1q_kernel(void* amps_, int n, int q, int kind, T c, T s) {
+  typedef typename CxT<T>::V V;
+  V* a = reinterpret_cast<V*>(amps_);
+  const long long half = 1ll << (n - 1);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long lo = ((i >> q) << (q + 1)) | (i & ((1ll << q) - 1));
+    const long long hi = lo | (1ll << q);
+    const V x = a[lo], y = a[hi];
+    V u, w;
+    if (kind == 0) {  // (x + y) * inv, (x - y) * inv
+      u.x = mul_rn(add_rn(x.x, y.x), c);
+      u.y = mul_rn(add_rn(x.y, y.y), c);
+      w.x = mul_rn(add_rn(x.x, -y.x), c);
+      w.y = mul_rn(add_rn(x.y, -y.y), c);
+    } else {  // c x + (-i s) y, (-i s) x + c y with s = sin(theta / 2)
+      u.x = add_rn(mul_rn(c, x.x), mul_rn(s, y.y));
+      u.y = add_rn(mul_rn(c, x.y), -mul_rn(s, y.x));
+      w.x = add_rn(mul_rn(s, x.y), mul_rn(c, y.x));
+      w.y = add_rn(-mul_rn(s, x.x), mul_rn(c, y.y));
+    }
+    a[lo] = u;
+    a[hi] = w;
+  }
+}
+
+// RZZ: equal bits i, j -> * e, differing -> * d (complex scalars)
+template <typename T>
+__global__ void rzz_kernel(void* amps_, int n, int i, int j, T er, T ei, T dr, T di) {
+  typedef typename CxT<T>::V V;
+  V* a = reinterpret_cast<V*>(amps_);
+  const long long N = 1ll << n;
+  for (long long z = blockIdx.x * (long long)blockDim.x + threadIdx.x; z < N; z += (long long)gridDim.x * blockDim.x) {
+    const bool differ = ((z >> i) ^ (z >> j)) & 1;
+    const T fr = differ ? dr : er, fi = differ ? di : ei;
+    const V x = a[z];
+    V y;
+    y.x = add_rn(mul_rn(x.x, fr), -mul_rn(x.y, fi));
+    y.y = add_rn(mul_rn(x.x, fi), mul_rn(x.y, fr));
+    a[z] = y;
+  }
+}
+
+// |0...0> (which = 0) or the uniform value v (which = 1)
+template <typename T>
+__global__ void reset_kernel(void* amps_, int n, int which, T v) {
+  typedef typename CxT<T>::V V;
+  V* a = reinterpret_cast<V*>(amps_);
+  const long long N = 1ll << n;
+  for (long long z = blockIdx.x * (long long)blockDim.x + threadIdx.x; z < N; z += (long long)gridDim.x * blockDim.x) {
+    V y;
+    y.x = which ? v : (z == 0 ? (T)1 : (T)0);
+    y.y = (T)0;
+    a[z] = y;
+  }
+}
+
 // Inverse-CDF draws for a batch of small distributions (noisy trajectories):
 // block b owns probs[b * N ...]; cdf = sequential cumsum, normalised by its
 // last element, first index with cdf > u (reference engine.py:254-263).

@@ -1252,6 +1252,57 @@ int lrq_run_fields(lrq_state* s, int p, const double* phase, const double* field
   return rc;
 }
 
+int lrq_reset(lrq_state* s, int which) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (s->world > 1) return fail(LRQ_EVALIDATION, "gate-by-gate execution is single-GPU");
+  if (which != 0 && which != 1) return fail(LRQ_EVALIDATION, "reset: 0 = |0...0>, 1 = uniform");
+  DeviceGuard guard(s->device);
+  const int grid = 4 * sm_count(s->device);
+  if (s->pbytes == 8) {
+    const float v = (float)(1.0 / sqrt((double)(1ull << s->n)));
+    reset_kernel<float><<<grid, 256, 0, s->stream>>>(s->amps, s->n, which, v);
+  } else {
+    const double v = 1.0 / sqrt((double)(1ull << s->n));
+    reset_kernel<double><<<grid, 256, 0, s->stream>>>(s->amps, s->n, which, v);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->ran = true;
+  s->reduced = false;
+  return LRQ_OK;
+}
+
+int lrq_apply_gate(lrq_state* s, int kind, int q0, int q1, double theta) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (s->world > 1) return fail(LRQ_EVALIDATION, "gate-by-gate execution is single-GPU");
+  const int n = s->n;
+  if (q0 < 0 || q0 >= n || (kind == 2 && (q1 < 0 || q1 >= n)))
+    return fail(LRQ_EVALIDATION, "qubit out of range for " + std::to_string(n) + " qubits");
+  if (kind == 2 && q0 == q1) return fail(LRQ_EVALIDATION, "RZZ qubits must differ");
+  if (kind < 0 || kind > 2) return fail(LRQ_EVALIDATION, "gate kind: 0 H, 1 RX, 2 RZZ");
+  if (kind != 0 && !isfinite(theta)) return fail(LRQ_EVALIDATION, "gate angle is not finite");
+  DeviceGuard guard(s->device);
+  const int grid = 4 * sm_count(s->device);
+  const bool f32 = s->pbytes == 8;
+  if (kind == 2) {
+    const double er = cos(-0.5 * theta), ei = sin(-0.5 * theta), dr = cos(0.5 * theta), di = sin(0.5 * theta);
+    if (f32)
+      rzz_kernel<float><<<grid, 256, 0, s->stream>>>(s->amps, n, q0, q1, (float)er, (float)ei, (float)dr, (float)di);
+    else
+      rzz_kernel<double><<<grid, 256, 0, s->stream>>>(s->amps, n, q0, q1, er, ei, dr, di);
+  } else {
+    const double c = kind == 0 ? 1.0 / sqrt(2.0) : cos(0.5 * theta), sn = kind == 0 ? 0.0 : sin(0.5 * theta);
+    if (f32)
+      gate1q_kernel<float><<<grid, 256, 0, s->stream>>>(s->amps, n, q0, kind, (float)c, (float)sn);
+    else
+      gate1q_kernel<double><<<grid, 256, 0, s->stream>>>(s->amps, n, q0, kind, c, sn);
+  }
+  CUDA_TRY(cudaGetLastError());
+  s->ran = true;
+  s->reduced = false;
+  return LRQ_OK;
+}
+
 int lrq_noisy_batch(int n, int pbytes, int device, int trajectories, int p, const double* phase,
                     const double* mixer, const unsigned* xmask, int64_t shots, const double* u, double* probs_out,
                     uint64_t* idx_out) {

@@ -151,12 +151,69 @@ def _device_state(num_qubits: int, precision: Precision, memory_budget: int | No
     return _native.DeviceState(num_qubits, precision.bytes_per_amplitude)
 
 
+_GATE_KIND = {"H": 0, "RX": 1, "RZZ": 2}
+
+
+def zero_state(num_qubits: int, precision: Precision | str = Precision.FP32,
+               memory_budget: int | None = None) -> StateVector:
+    """|0...0> in HBM (engine.py:99-110)."""
+    precision = Precision.coerce(precision)
+    dev = _device_state(num_qubits, precision, memory_budget)
+    dev.reset(0)
+    return StateVector(num_qubits, precision, dev)
+
+
+def init_plus_state(num_qubits: int, precision: Precision | str = Precision.FP32,
+                    memory_budget: int | None = None) -> StateVector:
+    """Uniform superposition with amplitude 2^(-n/2) (engine.py:113-121)."""
+    precision = Precision.coerce(precision)
+    dev = _device_state(num_qubits, precision, memory_budget)
+    dev.reset(1)
+    return StateVector(num_qubits, precision, dev)
+
+
+def _touch(sv: StateVector) -> None:
+    sv._amps = None  # host copy and reductions are stale after a gate
+    sv._cost = None
+
+
+def apply_h(sv: StateVector, q: int) -> None:
+    sv.device_state.apply_gate(0, q)
+    _touch(sv)
+
+
+def apply_rx(sv: StateVector, theta: float, q: int) -> None:
+    sv.device_state.apply_gate(1, q, 0, theta)
+    _touch(sv)
+
+
+def apply_rzz(sv: StateVector, theta: float, qa: int, qb: int) -> None:
+    sv.device_state.apply_gate(2, qa, qb, theta)
+    _touch(sv)
+
+
+def apply_gate(sv: StateVector, gate) -> None:
+    """One gate, one pass over the state on the GPU (engine.py:158-195)."""
+    q1 = gate.qubits[1] if len(gate.qubits) > 1 else 0
+    sv.device_state.apply_gate(_GATE_KIND[gate.kind], gate.qubits[0], q1, gate.theta or 0.0)
+    _touch(sv)
+
+
 def run_circuit(circuit: CircuitIR, precision: Precision | str = Precision.FP32,
                 memory_budget: int | None = None) -> StateVector:
-    """Evolve |0...0> through the circuit's H layer and p LR-QAOA layers on the GPU."""
+    """Evolve |0...0> through the circuit on the GPU.
+
+    H + p x (RZZ block, RX^n) circuits (everything build_circuit makes) run as
+    fused sweeps; any other gate list runs gate by gate (engine.py:198-207)."""
     precision = Precision.coerce(precision)
     check_memory(circuit.num_qubits, precision, memory_budget)
-    layers = lower_circuit(circuit)
+    try:
+        layers = lower_circuit(circuit)
+    except ValidationError:
+        sv = zero_state(circuit.num_qubits, precision, memory_budget)
+        for g in circuit.gates:
+            apply_gate(sv, g)
+        return sv
     dev = _device_state(circuit.num_qubits, precision, memory_budget)
     cost = getattr(circuit, "cost_weights", None)
     if cost is not None:

@@ -1,0 +1,66 @@
+"""GPU gate-by-gate execution (circuits that are not LR-QAOA shaped) against
+the reference engine's own amplitudes (tests/golden/gates.npz) and its
+known answers (test_engine.py:87-90)."""
+import numpy as np
+import pytest
+
+import paper_2604_26423_b200 as L
+from paper_2604_26423_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _engine():
+    from paper_2604_26423_b200.build import build
+    build()
+    assert _native.device_count() >= 1
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_random_gate_lists_match_reference(golden, case):
+    g = golden("gates.npz")
+    n, prec = int(g[f"n_{case}"]), str(g[f"prec_{case}"])
+    kinds, qa, qb = g[f"gates_{case}"]
+    names = ("H", "RX", "RZZ")
+    gates = []
+    for k, a, b, t in zip(kinds, qa, qb, g[f"theta_{case}"]):
+        k = int(k)
+        gates.append(L.GateOp(names[k], (int(a),) if k < 2 else (int(a), int(b)), None if k == 0 else float(t)))
+    sv = L.run_circuit(L.CircuitIR(num_qubits=n, gates=gates), prec)
+    want = g[f"amps_{case}"]
+    got = sv.amps
+    assert got.dtype == want.dtype
+    err = np.abs(got.astype(np.complex128) - want).max()
+    assert err <= (1e-13 if prec == "fp64" else 1e-6), err
+
+
+def test_rzz_pi_on_plus_state_known_answer():
+    sv = L.init_plus_state(2, "fp64")
+    L.apply_rzz(sv, np.pi, 0, 1)
+    np.testing.assert_allclose(sv.amps, [-0.5j, 0.5j, 0.5j, -0.5j], atol=1e-15)
+
+
+def test_gate_validation_and_reductions():
+    sv = L.zero_state(3, "fp64")
+    with pytest.raises(L.ValidationError):
+        L.apply_h(sv, 3)
+    with pytest.raises(L.ValidationError):
+        L.apply_rzz(sv, 0.1, 1, 1)
+    for q in range(3):
+        L.apply_h(sv, q)
+    inst = L.solve_instance(L.WmcInstance(3, ((0, 1, 0.5), (0, 2, 1.0), (1, 2, 0.25))))
+    # uniform distribution: exact r = (W/2) / C* (the random baseline)
+    assert L.exact_expected_r(sv, inst) == pytest.approx(L.random_baseline_expectation(inst), rel=1e-12)
+    assert sv.norm_squared() == pytest.approx(1.0, rel=1e-14)
+
+
+def test_large_state_gate_path_matches_fused_path():
+    # an LR-QAOA circuit with one extra gate takes the gate-by-gate path; without
+    # it the fused sweeps: the shared prefix agrees to rounding
+    inst = L.generate_instance(16, 3)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=2))
+    fused = L.run_circuit(circ, "fp64").amps
+    extra = L.CircuitIR(num_qubits=16, gates=list(circ.gates) + [L.GateOp("RX", (0,), 0.0)])
+    gated = L.run_circuit(extra, "fp64").amps
+    assert np.linalg.norm(gated - fused) / np.linalg.norm(fused) < 1e-12
