@@ -77,6 +77,12 @@ int lrq_run(lrq_state *s, int p, const double *phase, const double *mixer);
 int lrq_run_fields(lrq_state *s, int p, const double *phase, const double *field, const double *constant,
                    const double *mixer);
 
+/* lrq_run with per-qubit mixer half-angles mixer_q[k*n + q] that agree up to
+ * sign within each layer (noisy trajectories: Z/Y Paulis flip RX angles), and
+ * the X string left at the end of a trajectory: z <-> z ^ mask.  Single GPU. */
+int lrq_run_ex(lrq_state *s, int p, const double *phase, const double *mixer_q);
+int lrq_permute_xor(lrq_state *s, uint64_t mask);
+
 /* Gate-by-gate execution (engine.py:99-195) for circuits of any other shape:
  * reset to |0...0> (which = 0) or to the uniform state 2^(-n/2) (which = 1,
  * init_plus_state), then apply H (kind 0), RX(theta) (1) or RZZ(theta) (2)

@@ -42,6 +42,8 @@ _SIGNATURES = {
     "lrq_set_cost": ([_state_p, _p], _c_int),
     "lrq_run": ([_state_p, _c_int, _p, _p], _c_int),
     "lrq_run_fields": ([_state_p, _c_int, _p, _p, _p, _p], _c_int),
+    "lrq_run_ex": ([_state_p, _c_int, _p, _p], _c_int),
+    "lrq_permute_xor": ([_state_p, _c_u64], _c_int),
     "lrq_reset": ([_state_p, _c_int], _c_int),
     "lrq_apply_gate": ([_state_p, _c_int, _c_int, _c_int, _c_dbl], _c_int),
     "lrq_noisy_batch": ([_c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _c_i64, _p, _p, _p], _c_int),
@@ -262,6 +264,15 @@ class DeviceState:
         if field.size != p * self.n or constant.size != p:
             raise ValidationError(f"fields need shape ({p}, {self.n}) and constants ({p},)")
         check(lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
+
+    def run_ex(self, phase: np.ndarray, mixer_q: np.ndarray) -> None:
+        """run() with per-qubit mixer half-angles (p, n), equal up to sign per layer."""
+        phase = np.ascontiguousarray(phase, dtype=np.float64)
+        mixer_q = np.ascontiguousarray(mixer_q, dtype=np.float64)
+        check(lib().lrq_run_ex(self.handle, int(mixer_q.shape[0]), ptr(phase), ptr(mixer_q)))
+
+    def permute_xor(self, mask: int) -> None:
+        check(lib().lrq_permute_xor(self.handle, int(mask)))
 
     def reset(self, which: int = 0) -> None:
         check(lib().lrq_reset(self.handle, int(which)))

@@ -354,6 +354,21 @@ __global__ void rzz_kernel(void* amps_, int n, int i, int j, T er, T ei, T dr, T
   }
 }
 
+// a[z] <-> a[z ^ mask] (each pair swapped once, by the lower index)
+template <typename E>
+__global__ void xor_permute_kernel(void* data, int n, unsigned long long mask) {
+  E* a = reinterpret_cast<E*>(data);
+  const long long N = 1ll << n;
+  for (long long z = blockIdx.x * (long long)blockDim.x + threadIdx.x; z < N; z += (long long)gridDim.x * blockDim.x) {
+    const long long y = z ^ (long long)mask;
+    if (z < y) {
+      const E t = a[z];
+      a[z] = a[y];
+      a[y] = t;
+    }
+  }
+}
+
 // |0...0> (which = 0) or the uniform value v (which = 1)
 template <typename T>
 __global__ void reset_kernel(void* amps_, int n, int which, T v) {

@@ -174,6 +174,10 @@ struct lrq_state {
   double* dgather = nullptr;       // 4 * world doubles (all-gathered reductions)
   // optional per-layer Z fields / constant phases (lrq_run_fields)
   std::vector<double> field_h, cst_h;
+  // optional per-qubit mixer signs relative to the layer angle (lrq_run_ex)
+  std::vector<signed char> msign_h;
+  signed char* dmsign = nullptr;
+  size_t msign_cap = 0;
   double* dF = nullptr;
   int fcap = 0;
   std::vector<double> rank_sum_p;  // per-rank probability mass of the last run
@@ -199,6 +203,7 @@ void free_state(lrq_state* s) {
   cudaFree(s->stage);
   cudaFree(s->dWx);
   cudaFree(s->dF);
+  cudaFree(s->dmsign);
   cudaFree(s->dgather);
   if (s->comm && nccl().ok) nccl().CommDestroy(s->comm);
   if (s->group) {
@@ -254,6 +259,25 @@ MixerForm mixer_form(double h) {
     f.qim = s;
   }
   return f;
+}
+
+// tangents with per-qubit signs (lrq_run_ex): slot a of round r mixes qubit
+// sweep_qubit(...); returns the number of mixed qubits whose sign is -1
+int fill_tangents_signed(SweepParams& sp, int w, const PlanGroup& g, const PlanSweep& sw, int pair,
+                         const unsigned* masks, double t, const signed char* sign) {
+  int neg = 0;
+  for (int r = 0; r < sw.nrounds; ++r)
+    for (int a = 0; a < 5; ++a) {
+      double v = 0.0;
+      if ((masks[r] >> a) & 1u) {
+        const int q = sweep_qubit(g, sw, pair, r, a);
+        v = sign[q] < 0 ? -t : t;
+        neg += sign[q] < 0;
+      }
+      sp.tf[w][r][a] = (float)v;
+      sp.td[w][r][a] = v;
+    }
+  return neg;
 }
 
 void fill_tangents(SweepParams& sp, int w, const unsigned* masks, int nrounds, double t) {
@@ -1144,6 +1168,17 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.W = s->dW;  // zero until a cost is set: sum p is still reduced
     sp.F = fields ? s->dF : nullptr;
     sp.Fc = fields ? s->dF + (size_t)p * n : nullptr;
+    if (!s->msign_h.empty()) {
+      if (s->msign_h.size() > s->msign_cap) {
+        cudaFree(s->dmsign);
+        s->dmsign = nullptr;
+        CUDA_TRY(cudaMalloc(&s->dmsign, s->msign_h.size()));
+        s->msign_cap = s->msign_h.size();
+      }
+      CUDA_TRY(cudaMemcpyAsync(s->dmsign, s->msign_h.data(), s->msign_h.size(), cudaMemcpyHostToDevice, s->stream));
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+      sp.msign = s->dmsign;
+    }
     sp.init_re = init;
     sp.init_im = 0.0;
     sp.load = 0;
@@ -1169,15 +1204,26 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.num_tiles = s->num_tiles;
       sp.reduce = w.reduce ? 1 : 0;
       double sre = 1.0, sim = 0.0;
+      const bool signed_mix = !s->msign_h.empty();
       if (w.beta1 >= 0) {
         const MixerForm f = mixer_form(mixer[w.beta1]);
-        fill_tangents(sp, 0, w.mask1, w.nrounds, f.t);
+        int neg = 0;
+        if (signed_mix)
+          neg = fill_tangents_signed(sp, 0, g, w, pair_of(s->pbytes), w.mask1, f.t, &s->msign_h[(size_t)w.beta1 * n]);
+        else
+          fill_tangents(sp, 0, w.mask1, w.nrounds, f.t);
         cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
+        if (f.flip && (neg & 1)) sre = -sre, sim = -sim;  // (i s) per qubit: odd sign
       }
       if (w.beta2 >= 0) {
         const MixerForm f = mixer_form(mixer[w.beta2]);
-        fill_tangents(sp, 1, w.mask2, w.nrounds, f.t);
+        int neg = 0;
+        if (signed_mix)
+          neg = fill_tangents_signed(sp, 1, g, w, pair_of(s->pbytes), w.mask2, f.t, &s->msign_h[(size_t)w.beta2 * n]);
+        else
+          fill_tangents(sp, 1, w.mask2, w.nrounds, f.t);
         cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
+        if (f.flip && (neg & 1)) sre = -sre, sim = -sim;
       }
       sp.scale_re = sre;
       sp.scale_im = sim;
@@ -1250,6 +1296,45 @@ int lrq_run_fields(lrq_state* s, int p, const double* phase, const double* field
   s->field_h.clear();
   s->cst_h.clear();
   return rc;
+}
+
+int lrq_run_ex(lrq_state* s, int p, const double* phase, const double* mixer_q) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (s->world > 1) return fail(LRQ_EVALIDATION, "lrq_run_ex is single-GPU only");
+  if (p < 1 || !mixer_q) return fail(LRQ_EVALIDATION, "need p >= 1 and per-qubit mixer angles");
+  const int n = s->n;
+  std::vector<double> layer(p);
+  s->msign_h.assign((size_t)p * n, 1);
+  for (int k = 0; k < p; ++k) {
+    layer[k] = mixer_q[(size_t)k * n];
+    for (int q = 0; q < n; ++q) {
+      const double h = mixer_q[(size_t)k * n + q];
+      if (!isfinite(h) || fabs(h) != fabs(layer[k])) {
+        s->msign_h.clear();
+        return fail(LRQ_EVALIDATION, "per-qubit mixer angles of a layer must agree up to sign");
+      }
+      s->msign_h[(size_t)k * n + q] = (h == layer[k]) ? 1 : -1;
+    }
+  }
+  const int rc = lrq_run(s, p, phase, layer.data());
+  s->msign_h.clear();
+  return rc;
+}
+
+// z <-> z ^ mask (a Pauli-X string on the mask's qubits, up to phase)
+int lrq_permute_xor(lrq_state* s, uint64_t mask) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (s->world > 1) return fail(LRQ_EVALIDATION, "lrq_permute_xor is single-GPU only");
+  if (mask >> s->n) return fail(LRQ_EVALIDATION, "mask has bits above the state's qubits");
+  if (!mask) return LRQ_OK;
+  DeviceGuard guard(s->device);
+  const int grid = 4 * sm_count(s->device);
+  if (s->pbytes == 8) xor_permute_kernel<float2><<<grid, 256, 0, s->stream>>>(s->amps, s->n, mask);
+  else xor_permute_kernel<double2><<<grid, 256, 0, s->stream>>>(s->amps, s->n, mask);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->reduced = false;
+  return LRQ_OK;
 }
 
 int lrq_reset(lrq_state* s, int which) {

@@ -169,6 +169,13 @@ inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
   }
 }
 
+// global qubit behind tangent slot a of round r (the bit a of mask1/mask2)
+inline int sweep_qubit(const PlanGroup& g, const PlanSweep& w, int pair, int r, int a) {
+  const int tb = w.prog == 1 ? (wd_layout(w.kind, r) == 1 ? 7 : 2) + a + pair
+                             : reg_tile_bit(pair, prog_lo(g.kind, pair, w.kind, r), a);
+  return tb < g.m ? tb : g.q0 + (tb - g.m);
+}
+
 inline PlanSweep make_sweep(int group, int kind, int b1, int ph, int b2, bool red) {
   PlanSweep s;
   s.group = group;

@@ -16,8 +16,9 @@ trajectory back into an LR-QAOA circuit the engine runs fused:
 The random draws are the reference's own (Philox stream ("trajectory", t):
 ``fire`` then ``codes``), so trajectory t here is trajectory t there.  For
 n below the tile size all trajectories run in one launch, one CTA each
-(``lrq_noisy_batch``); larger n is refused (the reference's noisy workloads,
-e.g. acceptance #4, are n <= 12).
+(``lrq_noisy_batch``); above it each trajectory is one fused engine run with
+per-qubit mixer signs (``lrq_run_ex``) and the X string applied to the state
+(``lrq_permute_xor``).
 """
 from __future__ import annotations
 
@@ -162,14 +163,40 @@ def batch_programs(circuit: CircuitIR, cfg: DepolarizingConfig):
     return phase, mixer, xmask
 
 
+def _tile_bits(precision: Precision) -> int:
+    return 13 if precision is Precision.FP32 else 12
+
+
 def _batch(circuit: CircuitIR, cfg: DepolarizingConfig, precision: Precision, memory_budget, shots: int):
+    """(probs (T, 2^n) or None, indices (T, shots) or None) of every trajectory.
+
+    n below the tile: all trajectories in one lrq_noisy_batch launch.  Larger
+    n: one fused engine run per trajectory (lrq_run_ex, per-qubit mixer
+    signs), the X string applied to the state (lrq_permute_xor), then
+    probabilities or device draws."""
     n = circuit.num_qubits
     check_memory(n, precision, memory_budget)
     phase, mixer, xmask = batch_programs(circuit, cfg)
-    u = None
-    if shots:
-        u = np.stack([derive_rng(cfg.rng_seed, "shots", t).random(shots) for t in range(cfg.trajectories)])
-    return _native.noisy_batch(n, precision.bytes_per_amplitude, phase, mixer, xmask, u, want_probs=not shots)
+    us = [derive_rng(cfg.rng_seed, "shots", t).random(shots) for t in range(cfg.trajectories)] if shots else None
+    if n < _tile_bits(precision):
+        u = np.stack(us) if shots else None
+        return _native.noisy_batch(n, precision.bytes_per_amplitude, phase, mixer, xmask, u, want_probs=not shots)
+    dev = _native.DeviceState(n, precision.bytes_per_amplitude)
+    probs = None if shots else np.empty((cfg.trajectories, 1 << n))
+    idx = np.empty((cfg.trajectories, shots), dtype=np.uint64) if shots else None
+    try:
+        for t in range(cfg.trajectories):
+            dev.run_ex(phase[t], mixer[t])
+            dev.permute_xor(int(xmask[t]))
+            if shots:
+                dev.recompute()
+                idx[t] = dev.sample(us[t])
+            else:
+                a = dev.copy_amps().astype(np.complex128)
+                probs[t] = a.real ** 2 + a.imag ** 2
+    finally:
+        dev.close()
+    return probs, idx
 
 
 # ---------------------------------------------------------------------------
