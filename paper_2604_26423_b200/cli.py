@@ -1,11 +1,11 @@
-"""Command line for the GPU path: ``gen`` and noiseless ``simulate``.
+"""Command line for the GPU path: ``gen`` and ``simulate`` (noiseless and noisy).
 
 This is the ``lrqbench simulate`` integration of SURVEY §8(f) rank 1
 (cli.py:156-244 of the reference): the same arguments, results JSON keys,
 ``<out>.timing.csv`` for sharded runs and ``<out>.manifest.json``, with the
-circuit run by liblrq.so.  It does not cover the noisy mode, ``classify``,
-``bench``, ``fitnoise``, ``hqc`` or ``replay``, which are off the hot path
-(DESIGN.md §9).
+circuit run by liblrq.so; ``--mode noisy`` runs the GPU trajectories
+(noise.py).  ``classify``, ``bench``, ``fitnoise``, ``hqc`` and ``replay``
+are off the hot path.
 
     python -m paper_2604_26423_b200 gen --n 26 --out inst.json --solve-limit 26
     python -m paper_2604_26423_b200 simulate --instance inst.json --out res.json --p 3 --precision fp64
@@ -26,8 +26,11 @@ from pathlib import Path
 from . import __version__
 from .circuit import LrQaoaParams, build_circuit, gate_counts
 from .engine import exact_expected_r, run_circuit, sample, save_statevector
+from .noise import DepolarizingConfig, epsilon_accumulated, r_overlap, run_noisy_ensemble
 from .errors import AbortedRunError, CapacityError, StateError, ValidationError
-from .problem import approximation_ratio, generate_instance, load_instance, save_instance, solve_instance
+from .problem import (approximation_ratio, generate_instance, load_instance, random_baseline_expectation,
+                      save_instance, solve_instance)
+from .rng import derive_seed
 from .sharded import plan_for_shard_count, run_circuit_sharded, write_timing_csv
 
 EXIT_OK, EXIT_VALIDATION, EXIT_CAPACITY, EXIT_RUNTIME = 0, 2, 3, 4
@@ -74,8 +77,6 @@ def _cmd_gen(args) -> int:
 
 
 def _cmd_simulate(args) -> int:
-    if args.mode != "noiseless":
-        raise ValidationError("the GPU backend runs the noiseless mode only (noisy trajectories: SURVEY §8(f) 2)")
     inst = load_instance(args.instance)
     db = args.delta if args.delta_beta is None else args.delta_beta
     dg = args.delta if args.delta_gamma is None else args.delta_gamma
@@ -85,6 +86,8 @@ def _cmd_simulate(args) -> int:
     payload = {"n": inst.num_vertices, "p": args.p, "delta_beta": db, "delta_gamma": dg, "seed": args.seed,
                "precision": args.precision, "n_1q": n_1q, "n_2q": n_2q, "mode": args.mode}
     outputs = [args.out]
+    if args.mode == "noisy":
+        return _simulate_noisy(args, inst, circuit, n_2q, solved, payload, outputs)
     if args.shards > 1:
         plan = plan_for_shard_count(inst.num_vertices, args.shards)
         sv, record = run_circuit_sharded(circuit, plan, args.precision, args.memory_bytes)
@@ -106,6 +109,33 @@ def _cmd_simulate(args) -> int:
         save_statevector(sv, args.dump_state)
         outputs.append(args.dump_state)
     sv.release()
+    args.out.write_text(json.dumps(payload, indent=2, sort_keys=True) + "\n")
+    _manifest(args, [args.instance], outputs)
+    shown = "n/a" if payload["mean_r"] is None else f"{payload['mean_r']:.4f}"
+    print(f"wrote {args.out}: mode={args.mode} mean_r={shown}")
+    return EXIT_OK
+
+
+def _simulate_noisy(args, inst, circuit, n_2q, solved, payload, outputs) -> int:
+    """cli.py:195-232 of the reference: pooled trajectory shots, and against
+    the ideal and random baselines the overlap ratio."""
+    cfg = DepolarizingConfig(epsilon=args.epsilon, trajectories=args.trajectories, rng_seed=args.seed)
+    shots = run_noisy_ensemble(circuit, cfg, args.shots, args.precision, args.memory_bytes)
+    mean_r = approximation_ratio(inst, shots) if solved else None
+    ovl = None
+    if solved:
+        ideal = run_circuit(circuit, args.precision, args.memory_bytes)
+        if args.ideal_shots is None:
+            r_ideal = exact_expected_r(ideal, inst)
+        else:
+            r_ideal = approximation_ratio(inst, sample(ideal, args.ideal_shots, derive_seed(args.seed, "ideal")))
+        ideal.release()
+        r_random = random_baseline_expectation(inst)
+        ovl = r_overlap(mean_r, r_random, r_ideal)
+        payload.update({"r_ideal": r_ideal, "r_random": r_random})
+    payload.update({"epsilon": args.epsilon, "trajectories": args.trajectories, "shots": args.shots,
+                    "eps_acc": epsilon_accumulated(n_2q, args.epsilon), "mean_r": mean_r, "r_ovl": ovl,
+                    "bitstrings": shots.bitstrings()})
     args.out.write_text(json.dumps(payload, indent=2, sort_keys=True) + "\n")
     _manifest(args, [args.instance], outputs)
     shown = "n/a" if payload["mean_r"] is None else f"{payload['mean_r']:.4f}"
@@ -142,6 +172,10 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--shots", type=int, default=100)
     s.add_argument("--shards", type=int, default=1)
     s.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
+    s.add_argument("--epsilon", type=float, default=0.0, help="two-qubit depolarizing rate")
+    s.add_argument("--trajectories", type=int, default=1)
+    s.add_argument("--ideal-shots", type=int, default=None,
+                   help="estimate the ideal baseline from this many shots instead of exactly")
     s.add_argument("--dump-state", type=Path, default=None)
     s.add_argument("--memory-bytes", type=int, default=None)
     common(s)

@@ -23,7 +23,8 @@ def test_gen_without_solve_matches_reference_instance(tmp_path):
 def test_simulate_input_errors_exit_2(tmp_path, capsys):
     assert main(["simulate", "--instance", str(tmp_path / "missing.json"), "--out", str(tmp_path / "r.json")]) == 2
     inst = os.path.join(GOLDEN, "cli_n12_inst.json")
-    assert main(["simulate", "--instance", inst, "--out", str(tmp_path / "r.json"), "--mode", "noisy"]) == 2
-    assert "noiseless mode only" in capsys.readouterr().err
+    assert main(["simulate", "--instance", inst, "--out", str(tmp_path / "r.json"), "--mode", "noisy",
+                 "--epsilon", "1.5"]) == 2
+    assert "epsilon must lie in [0, 1]" in capsys.readouterr().err
     with pytest.raises(SystemExit):
         main(["simulate", "--instance", inst, "--out", str(tmp_path / "r.json"), "--precision", "fp16"])
