@@ -116,8 +116,10 @@ int lrq_recompute(lrq_state *s);
  * (the reference draws them from Philox("shots", 0) on the host).           */
 int lrq_sample(lrq_state *s, const double *u, int64_t shots, uint64_t *idx_out);
 
-/* amplitudes [start, start+count) -> host, complex64/complex128 interleaved. */
+/* amplitudes [start, start+count) -> host, complex64/complex128 interleaved;
+ * lrq_store_amps: host -> state (LQSV load, engine.py:296-312).           */
 int lrq_copy_amps(lrq_state *s, uint64_t start, uint64_t count, void *host_out);
+int lrq_store_amps(lrq_state *s, uint64_t start, uint64_t count, const void *host_in);
 
 /* bit-exact cut values (problem.py:139-149) on the device. z==NULL means the
  * contiguous range [start, start+count).                                    */

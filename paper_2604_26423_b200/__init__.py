@@ -16,7 +16,9 @@ from .circuit import (
     Schedule,
     build_circuit,
     build_schedule,
+    circuit_to_text,
     gate_counts,
+    hqc_cost,
     lower_circuit,
 )
 from .engine import (
@@ -26,6 +28,7 @@ from .engine import (
     apply_rx,
     apply_rzz,
     init_plus_state,
+    load_statevector,
     zero_state,
     ShotSet,
     StateVector,

@@ -51,6 +51,7 @@ _SIGNATURES = {
     "lrq_recompute": ([_state_p], _c_int),
     "lrq_sample": ([_state_p, _p, _c_i64, _p], _c_int),
     "lrq_copy_amps": ([_state_p, _c_u64, _c_u64, _p], _c_int),
+    "lrq_store_amps": ([_state_p, _c_u64, _c_u64, _p], _c_int),
     "lrq_cut_values": ([_c_int, _p, _p, _c_u64, _c_i64, _p, _c_int], _c_int),
     "lrq_max_cut": ([_c_int, _p, _c_int, ctypes.POINTER(_c_u64), ctypes.POINTER(_c_dbl)], _c_int),
     "lrq_set_timing": ([_state_p, _c_int], _c_int),
@@ -301,6 +302,11 @@ class DeviceState:
         out = np.empty(count, dtype=dt)
         check(lib().lrq_copy_amps(self.handle, start, count, ptr(out)))
         return out
+
+    def store_amps(self, amps: np.ndarray, start: int = 0) -> None:
+        dt = np.complex64 if self.precision_bytes == 8 else np.complex128
+        amps = np.ascontiguousarray(amps, dtype=dt)
+        check(lib().lrq_store_amps(self.handle, int(start), int(amps.size), ptr(amps)))
 
     def set_timing(self, on: bool) -> None:
         check(lib().lrq_set_timing(self.handle, 1 if on else 0))

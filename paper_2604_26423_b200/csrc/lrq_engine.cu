@@ -1651,6 +1651,18 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   return LRQ_OK;
 }
 
+int lrq_store_amps(lrq_state* s, uint64_t start, uint64_t count, const void* host) {
+  if (!s || (!host && count)) return fail(LRQ_EVALIDATION, "null argument");
+  if (start + count > (1ull << s->n)) return fail(LRQ_EVALIDATION, "amplitude range out of bounds");
+  DeviceGuard guard(s->device);
+  CUDA_TRY(cudaMemcpyAsync((char*)s->amps + start * s->pbytes, host, count * s->pbytes, cudaMemcpyHostToDevice,
+                           s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->ran = true;
+  s->reduced = false;
+  return LRQ_OK;
+}
+
 int lrq_copy_amps(lrq_state* s, uint64_t start, uint64_t count, void* host) {
   if (!s || (!host && count)) return fail(LRQ_EVALIDATION, "null argument");
   if (start + count > (1ull << s->n)) return fail(LRQ_EVALIDATION, "amplitude range out of bounds");

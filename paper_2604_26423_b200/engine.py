@@ -298,6 +298,28 @@ def save_statevector(sv: StateVector, path: str | Path) -> None:
             fh.write(np.ascontiguousarray(part, dtype=code).tobytes())
 
 
+def load_statevector(path: str | Path, memory_budget: int | None = None) -> StateVector:
+    """LQSV dump -> a state in HBM (engine.py:296-312), streamed in chunks."""
+    raw = Path(path).read_bytes()
+    if len(raw) < _HEADER.size:
+        raise ValidationError(f"{path} is not a statevector dump (truncated header)")
+    magic, version, fbytes, n = _HEADER.unpack_from(raw)
+    if magic != _MAGIC or version != 1:
+        raise ValidationError(f"{path} is not a statevector dump (bad magic/version)")
+    if fbytes not in (4, 8):
+        raise ValidationError(f"{path} has unsupported float width {fbytes}")
+    precision = Precision.FP32 if fbytes == 4 else Precision.FP64
+    code = "<c8" if fbytes == 4 else "<c16"
+    amps = np.frombuffer(raw, dtype=code, offset=_HEADER.size)
+    if amps.size != 1 << n:
+        raise ValidationError(f"{path} payload has {amps.size} amplitudes, expected {1 << n}")
+    dev = _device_state(n, precision, memory_budget)
+    chunk = 1 << 24
+    for lo in range(0, amps.size, chunk):
+        dev.store_amps(amps[lo:lo + chunk], lo)
+    return StateVector(n, precision, dev)
+
+
 def load_statevector_amps(path: str | Path) -> tuple[int, np.ndarray]:
     """Read an LQSV dump into host memory: (num_qubits, amplitudes)."""
     raw = Path(path).read_bytes()

@@ -28,3 +28,12 @@ def test_simulate_input_errors_exit_2(tmp_path, capsys):
     assert "epsilon must lie in [0, 1]" in capsys.readouterr().err
     with pytest.raises(SystemExit):
         main(["simulate", "--instance", inst, "--out", str(tmp_path / "r.json"), "--precision", "fp16"])
+
+
+def test_circuit_text_and_cost_model_match_reference():
+    import paper_2604_26423_b200 as L
+    circ = L.build_circuit(L.generate_instance(5, 1), L.LrQaoaParams(p=2))
+    assert L.circuit_to_text(circ) == open(os.path.join(GOLDEN, "circuit_n5.txt")).read()
+    assert L.hqc_cost(160, 2340, 40, 10) == pytest.approx(52.52)
+    with pytest.raises(L.ValidationError):
+        L.hqc_cost(1, 1, 1, 0)

@@ -64,3 +64,20 @@ def test_large_state_gate_path_matches_fused_path():
     extra = L.CircuitIR(num_qubits=16, gates=list(circ.gates) + [L.GateOp("RX", (0,), 0.0)])
     gated = L.run_circuit(extra, "fp64").amps
     assert np.linalg.norm(gated - fused) / np.linalg.norm(fused) < 1e-12
+
+
+@pytest.mark.parametrize("name,n,seed,p,prec", [("lqsv_n8_fp64.bin", 8, 2, 3, "fp64"), ("lqsv_n9_fp32.bin", 9, 3, 2, "fp32")])
+def test_lqsv_load_of_reference_dump_and_round_trip(tmp_path, name, n, seed, p, prec):
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)
+    ref = L.load_statevector(path)
+    assert ref.num_qubits == n and ref.precision is L.Precision.coerce(prec)
+    mine = L.run_circuit(L.build_circuit(L.generate_instance(n, seed), L.LrQaoaParams(p=p)), prec)
+    tol = 1e-12 if prec == "fp64" else 1e-6
+    assert np.abs(ref.amps.astype(np.complex128) - mine.amps).max() < tol
+    out = tmp_path / "s.bin"
+    L.save_statevector(ref, out)
+    assert out.read_bytes() == open(path, "rb").read()  # byte-identical dump of the loaded state
+    # the loaded state is a live device state: reductions and sampling work on it
+    inst = L.solve_instance(L.generate_instance(n, seed))
+    assert L.exact_expected_r(ref, inst) == pytest.approx(L.exact_expected_r(mine, inst), rel=1e-5)
