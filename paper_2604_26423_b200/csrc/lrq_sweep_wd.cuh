@@ -65,6 +65,9 @@ struct WdSweep {
   static constexpr int MA = group_ma(GK, PAIR);  // run amp bits
   static constexpr int MU = MA - PAIR;           // run unit bits (>= 2)
   static constexpr int SWM = (GK == GK_H && PAIR) ? 3 : 7;
+  // L2 register bits k hold unit bits 2 + k; those below MU are run bits,
+  // never targets: no butterflies for them (H4 c64: bit 2; H c128: bits 2, 3)
+  static constexpr unsigned L2MASK = 31u & ~((1u << (MU > 2 ? MU - 2 : 0)) - 1u);
   static constexpr bool PH = SK == SK_F || SK == SK_P;  // has a cost phase
   static constexpr bool INIT = SK == SK_P;              // no load: H|0> value
 
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       // L2: lane = unit bits 7..11, registers = unit bits 2..6
 #pragma unroll
       for (int a = 0; a < 32; ++a) r[a] = rg[W::slot(a, lane)];
-      W::template mix<31u>(r, P.tf[0][1], P.td[0][1]);
+      W::template mix<W::L2MASK>(r, P.tf[0][1], P.td[0][1]);
     } else {
       team_sync_n(1 + team, kWdWarps * 32);  // warp 0's tile fields are visible
     }
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       for (int a = 0; a < RA; ++a) F[a] = hb[W::reg_bit(2, a)] + thr[a * kWdTT + tt2];
       const double2 sc = INIT ? cmul(scale, make_double2(P.init_re, P.init_im)) : scale;
       W::phase(r, C, F, sc, PRR);
-      W::template mix<31u>(r, P.tf[1][RPH], P.td[1][RPH]);
+      W::template mix<W::L2MASK>(r, P.tf[1][RPH], P.td[1][RPH]);
     }
     // back to L1 (conflict-free against the TMA layout) through the region
     __syncwarp();
