@@ -410,24 +410,27 @@ bool use_tma_path(int pbytes, int gk, int sk) {
   return pbytes == 8 && gk != GK_A && (sk == SK_M || sk == SK_F);
 }
 
-template <typename T, int GK, int SK>
+template <typename T, int GK, int SK, int TEAMS>
 int launch_wd_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(sweep_wd_kernel<T, GK, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    err = cudaFuncSetAttribute(sweep_wd_kernel<T, GK, SK, TEAMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024);
   });
   CUDA_TRY(err);
-  sweep_wd_kernel<T, GK, SK><<<grid, kWdThreads, smem, st>>>(sp);
+  sweep_wd_kernel<T, GK, SK, TEAMS><<<grid, TEAMS * kWdWarps * 32, smem, st>>>(sp);
   CUDA_TRY(cudaGetLastError());
   return LRQ_OK;
 }
 
+// P (no load, light on registers) runs three tiles in flight, each team on
+// its own stage; M and F keep two so their threads get 255 registers
 template <typename T, int GK>
 int launch_wd_kind(cudaStream_t st, int sk, const SweepParams& sp, int grid, size_t smem) {
-  if (sk == SK_F) return launch_wd_t<T, GK, SK_F>(st, sp, grid, smem);
-  if (sk == SK_P) return launch_wd_t<T, GK, SK_P>(st, sp, grid, smem);
-  return launch_wd_t<T, GK, SK_M>(st, sp, grid, smem);
+  if (sk == SK_F) return launch_wd_t<T, GK, SK_F, 2>(st, sp, grid, smem);
+  if (sk == SK_P) return launch_wd_t<T, GK, SK_P, 3>(st, sp, grid, smem);
+  return launch_wd_t<T, GK, SK_M, 2>(st, sp, grid, smem);
 }
 
 // warp-decoupled high-group sweep (plan prog 1): TMA ring of 3 stages, 2

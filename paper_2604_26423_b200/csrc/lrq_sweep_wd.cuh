@@ -34,9 +34,8 @@
 
 namespace lrq {
 
-constexpr int kWdTeams = 2;  // tiles in flight per CTA
-constexpr int kWdWarps = 4;  // warps per tile
-constexpr int kWdThreads = kWdTeams * kWdWarps * 32;  // no producer warp (see refill)
+constexpr int kWdTeamsMax = 3;  // tiles in flight per CTA: 2 (M, F: 255 registers) or 3 (P)
+constexpr int kWdWarps = 4;     // warps per tile
 constexpr int kWdTT = kWdWarps * 32;  // tile threads
 constexpr int kWdRAmax = 6;           // register amp bits: (pair) + 5 unit bits
 // a stage holds the 64 KB TMA tile plus 2 KB so that, after the tile is read,
@@ -49,7 +48,7 @@ __host__ __device__ inline size_t wd_smem_bytes(int n, int nst, bool usesJ) {
   if (usesJ) b = align16(b + 8 * (size_t)(n * n + n));
   b += 8 * (size_t)((kWdRAmax + 1) * kWdTT);  // per-tile-thread constants
   b += 16 * 64;                               // PRR (float2 x 64 or double2 x 32)
-  b += 8 * (size_t)(kWdTeams * 16);  // per-team hb[13] + ebb
+  b += 8 * (size_t)(kWdTeamsMax * 16);  // per-team hb[13] + ebb
   b += 4 * 64;                         // block-bit list
   return align16(b) + 1024;
 }
@@ -209,9 +208,11 @@ struct WdSweep {
   }
 };
 
-template <typename T, int GK, int SK>
-__global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_constant__ SweepParams P) {
+template <typename T, int GK, int SK, int TEAMS>
+__global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(const __grid_constant__ SweepParams P) {
   typedef WdSweep<T, GK, SK> W;
+  constexpr int kWdTeams = TEAMS;
+  constexpr int kWdThreads = TEAMS * kWdWarps * 32;
   typedef typename W::U U;
   constexpr int MA = W::MA, MU = W::MU, KA = W::KA, RA = W::RA, NV = W::NV, PAIR = W::PAIR;
   constexpr bool PH = W::PH, INIT = W::INIT;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
   const int nst = P.nstages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* stages = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * kWdStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * kWdStageBytes);  // nst * teams <= 16
   unsigned char* sp = smem + (size_t)nst * kWdStageBytes + 128;
   double *Jm = nullptr, *Jx = nullptr;
   if (PH) {
@@ -356,7 +357,8 @@ __global__ void __launch_bounds__(kWdThreads, 1) sweep_wd_kernel(const __grid_co
       }
     }
 
-    mbar_wait(&full[s * kWdTeams + team], (unsigned)((k / (nst * kWdTeams)) & 1));
+    // the k-th tile is the (k / lcm(nst, teams))-th use of its (stage, team) barrier
+    mbar_wait(&full[s * kWdTeams + team], (unsigned)((k / (nst % kWdTeams == 0 ? nst : nst * kWdTeams)) & 1));
     if constexpr (!INIT) {
       // L1: lane = unit bits 2..6, registers = unit bits 7..11 (TMA layout)
 #pragma unroll
