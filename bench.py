@@ -170,9 +170,10 @@ def kernel_launches(kinds, n_local, tile_bits=13):
     """Our kernel launches behind the engine's timing records: one per sweep
     ('P','M','F','R','Q'), three for the multi-CTA finalize ('Z', tile count
     >= 8192), two for a deferred-flip reversal ('X'); remaps ('T') are NCCL
-    send/recv plus copies, not our kernels."""
+    send/recv plus copies, and a fused remap ('Y') is the preceding sweep's own
+    stores plus a one-float NCCL all-reduce barrier: neither is our kernel."""
     z = 3 if (1 << max(0, n_local - tile_bits)) >= 8192 else 1
-    return sum(z if k == "Z" else 2 if k == "X" else 0 if k == "T" else 1 for k in kinds)
+    return sum(z if k == "Z" else 2 if k == "X" else 0 if k in "TY" else 1 for k in kinds)
 
 
 def cpu_reference(n, p, precision, budget_s, seed):
@@ -355,7 +356,7 @@ def run_ours_dist(args, rank, world, local_rank, dist):
     import paper_2604_26423_b200 as L
     from paper_2604_26423_b200 import _native
     from paper_2604_26423_b200.build import build
-    from paper_2604_26423_b200.distributed import drain_dist_pool, run_circuit_distributed
+    from paper_2604_26423_b200.distributed import drain_dist_pool, enable_fused_remap, run_circuit_distributed
 
     if rank == 0:
         build()
@@ -379,6 +380,7 @@ def run_ours_dist(args, rank, world, local_rank, dist):
     box = [_native.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(box, src=0)
     dev = _native.DeviceState.create_dist(n, B, dev_index, rank, world, box[0])
+    fused = enable_fused_remap(dev)
     dev.set_cost(w)
     stream = torch.cuda.ExternalStream(dev.stream())
     for _ in range(args.warmup):
@@ -430,7 +432,7 @@ def run_ours_dist(args, rank, world, local_rank, dist):
     alg = sum((1 if k in "PQ" else 2) * (B << nl) for _, k in sw)
     sweep_time_s = sum(m for m, _ in sw) * 1e-3
     achieved = alg / sweep_time_s / 1e9
-    remap_ms = [m for m, k in zip(ms_all, kinds_all) if k == "T"]
+    remap_ms = [m for m, k in zip(ms_all, kinds_all) if k in "TY"]
     remap_bytes = (world - 1) * (B << (nl - g))  # sent (= received) per GPU per remap
     peak, peak_kind = measured_peak()
     amp_updates = float(1 << n) * p * args.steps
@@ -464,7 +466,8 @@ def run_ours_dist(args, rank, world, local_rank, dist):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_kind, "traffic": None, "kernel": "sweep_kernel (local shard)",
                      "bytes_per_launch": 2 * (B << nl), "launch_ms_avg": sweep_time_s * 1e3 / max(1, len(sw))},
-        "remap": {"per_step": len(remap_ms) // args.steps, "ms_avg": statistics.mean(remap_ms) if remap_ms else None,
+        "remap": {"mode": "fused into the group-A sweep (peer stores over NVLink)" if fused else "NCCL send/recv",
+                  "per_step": len(remap_ms) // args.steps, "ms_avg": statistics.mean(remap_ms) if remap_ms else None,
                   "bytes_sent_per_gpu": remap_bytes,
                   "algbw_GBps": remap_bytes / (statistics.mean(remap_ms) * 1e-3) / 1e9 if remap_ms else None},
         "sweep_ms": {k: round(statistics.mean(m for m, kk in sw if kk == k), 3) for k in sorted(set(kinds_all))

@@ -141,6 +141,17 @@ int lrq_create_dist(int num_qubits, int precision_bytes, int device, int rank, i
                     uint64_t memory_budget, lrq_state **out);
 int lrq_dist_info(lrq_state *s, int *n_local, int *rank, int *world);
 
+/* Fused remap over peer memory (NVLink): each rank keeps two state buffers and
+ * the sweep before a remap stores every block straight into its owner rank's
+ * next buffer, so the all-to-all rides on the sweep.  Collective setup: every
+ * rank exports its two buffers (lrq_ipc_handles, 128 bytes), the host gathers
+ * them in rank order (world * 128 bytes) and every rank calls lrq_fused_setup,
+ * which maps the peers' buffers and runs a peer-store self-test; *enabled = 1
+ * on all ranks or on none (then the NCCL remap is used).  In-process shard
+ * groups use the members' buffers directly.  LRQ_FUSED_REMAP=0 disables.   */
+int lrq_ipc_handles(lrq_state *s, void *out, size_t cap);
+int lrq_fused_setup(lrq_state *s, const void *all_handles, int *enabled);
+
 /* in-process shards — the B200 form of the reference's thread-per-shard
  * engine (run_circuit_sharded / _ShardWorker, sharded.py:200-385): `world`
  * shard states in ONE process, one host thread per shard making the same

@@ -64,6 +64,8 @@ _SIGNATURES = {
     "lrq_group_destroy": ([_p], _c_int),
     "lrq_group_abort": ([_p], _c_int),
     "lrq_create_shard": ([_c_int, _c_int, _c_int, _c_int, _p, _c_u64, ctypes.POINTER(_state_p)], _c_int),
+    "lrq_ipc_handles": ([_state_p, _p, ctypes.c_size_t], _c_int),
+    "lrq_fused_setup": ([_state_p, _p, ctypes.POINTER(_c_int)], _c_int),
     "lrq_dist_info": ([_state_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
     "lrq_describe_dist_plan": ([_c_int, _c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
     "lrq_dist_terms": ([_c_int, _c_int, _c_int, _c_int, _p, _p, _p, ctypes.POINTER(_c_dbl)], _c_int),
@@ -215,6 +217,18 @@ class DeviceState:
         self.n_local = n - (group.world.bit_length() - 1)
         self._dist = True
         return self
+
+    def ipc_handles(self) -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib().lrq_ipc_handles(self.handle, buf, 128))
+        return buf.raw
+
+    def fused_setup(self, all_handles: bytes) -> bool:
+        """Collective: map the peers' state buffers for the fused remap."""
+        buf = ctypes.create_string_buffer(all_handles, len(all_handles))
+        on = _c_int(0)
+        check(lib().lrq_fused_setup(self.handle, buf, ctypes.byref(on)))
+        return bool(on.value)
 
     def close(self, park: bool = True) -> None:
         """Release the state (distributed shards are never parked)."""

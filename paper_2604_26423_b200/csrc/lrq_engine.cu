@@ -166,6 +166,14 @@ struct lrq_state {
   int world = 1, rank = 0, g = 0, n_total = 0;
   ncclComm_t comm = nullptr;
   lrq_group* group = nullptr;      // in-process transport (lrq_create_shard)
+  // fused remap: two state buffers per rank (amps == bufs[cur]); the sweep
+  // before a remap writes the next buffer of every rank through peer pointers
+  void* bufs[2] = {nullptr, nullptr};
+  int cur = 0;
+  void* peer[2][8] = {};
+  bool fused = false;
+  std::vector<void*> ipc_open;  // peer buffers mapped with cudaIpcOpenMemHandle
+  float* dflag = nullptr;       // 1 float for the NCCL stream barrier
   unsigned char* stage = nullptr;  // remap staging, (world-1) * chunk bytes
   size_t chunk = 0;
   std::vector<double> cost_edges;  // global cost edges (lexicographic)
@@ -189,7 +197,14 @@ namespace {
 void free_state(lrq_state* s) {
   if (!s) return;
   DeviceGuard g(s->device);
-  cudaFree(s->amps);
+  for (void* p : s->ipc_open) cudaIpcCloseMemHandle(p);
+  if (s->bufs[1]) {
+    cudaFree(s->bufs[0]);
+    cudaFree(s->bufs[1]);
+  } else {
+    cudaFree(s->amps);
+  }
+  cudaFree(s->dflag);
   cudaFree(s->red);
   cudaFree(s->prefix);
   cudaFree(s->out);
@@ -675,6 +690,42 @@ int exchange_blocks(lrq_state* s, int peer) {
   return LRQ_OK;
 }
 
+// fused remap availability: both state buffers on every rank and the peers'
+// buffers addressable (in-process groups: the members' pointers, with peer
+// access across devices; NCCL ranks: mapped by lrq_fused_setup)
+bool fused_ready(lrq_state* s) {
+  if (!s->bufs[1] || !env_int("LRQ_FUSED_REMAP", 1)) return false;
+  if (s->group) {
+    lrq_group* G = s->group;
+    for (int b = 0; b < s->world; ++b) {
+      lrq_state* o = G->members[b];
+      if (!o || !o->bufs[1] || o->cur != s->cur) return false;
+      if (o->device != s->device) {
+        int ok = 0;
+        if (cudaDeviceCanAccessPeer(&ok, s->device, o->device) != cudaSuccess || !ok) return false;
+        cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return false;
+        cudaGetLastError();
+      }
+      s->peer[0][b] = o->bufs[0];
+      s->peer[1][b] = o->bufs[1];
+    }
+    return true;
+  }
+  return s->fused;
+}
+
+// all ranks' fused-remap stores are complete before anyone reads its buffer
+int fused_barrier(lrq_state* s) {
+  if (s->group) {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return group_barrier(s->group);
+  }
+  // stream-ordered: the all-reduce completes only after every rank's sweep
+  NCCL_TRY(nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));
+  return LRQ_OK;
+}
+
 // lrq_run for world > 1 (make_dist_plan): local sweeps in the permutation
 // state each one records, remaps between layers, final read-only reduction.
 int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
@@ -711,6 +762,7 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
   const int grid = (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap);
   int flips = 0;
   for (int k = 0; k < p; ++k) flips += mixer_form(mixer[k]).flip;
+  const bool fused = fused_ready(s);
   for (const PlanSweep& w : P.sweeps) {
     const PlanGroup& gr = P.groups[w.group];
     if (w.kind == SK_Q && (flips & 1)) {
@@ -758,10 +810,33 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
-    int rc = w.prog == 1 ? launch_wd(s, gr.kind, w.kind, sp) : launch_sweep(s, gr.kind, w.kind, sp, grid);
+    const bool fuse = w.remap_after && fused && gr.kind == GK_A && w.kind == SK_M;
+    if (fuse) {
+      // the sweep stores block b of its output into rank b's next buffer at
+      // this rank's block: the remap rides on the sweep's own stores
+      const int next = 1 - s->cur;
+      const size_t blockBytes = (size_t)s->pbytes << (nl - g);
+      int tb = 0;
+      while ((1ll << tb) < s->num_tiles) ++tb;
+      sp.remap = 1;
+      sp.rbits = tb - g;
+      for (int b = 0; b < s->world; ++b) sp.rdst[b] = (char*)s->peer[next][b] + (size_t)s->rank * blockBytes;
+    }
+    int rc = w.prog == 1 ? launch_wd(s, gr.kind, w.kind, sp)
+             : fuse      ? (s->pbytes == 8 ? launch_sweep_kind<float>(s->stream, gr.kind, w.kind, sp, grid,
+                                                                       sweep_smem_bytes(nl, true, false, false))
+                                           : launch_sweep_kind<double>(s->stream, gr.kind, w.kind, sp, grid,
+                                                                        sweep_smem_bytes(nl, true, false, false)))
+                         : launch_sweep(s, gr.kind, w.kind, sp, grid);
     if (rc) return rc;
     record(s, ev++, "PMFRLQN"[w.kind]);
-    if (w.remap_after) {
+    if (fuse) {
+      rc = fused_barrier(s);  // every rank's stores into our next buffer are done
+      if (rc) return rc;
+      s->cur = 1 - s->cur;
+      s->amps = s->bufs[s->cur];
+      record(s, ev++, 'Y');
+    } else if (w.remap_after) {
       rc = exchange_blocks(s, -1);
       if (rc) return rc;
       record(s, ev++, 'T');
@@ -971,10 +1046,21 @@ int create_rank_state(int n_total, int pbytes, int device, int rank, int world, 
   if (e == cudaSuccess) e = cudaMalloc(&s->dWx, sizeof(double) * nl);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->dWx, 0, sizeof(double) * nl, s->stream);
   if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * 4 * world);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dflag, sizeof(float));
   if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) {
     free_state(s);
     return fail(LRQ_ECAPACITY, std::string("distributed buffers: ") + cudaGetErrorString(e));
+  }
+  // second state buffer for the fused remap, if it fits (else NCCL/swap remaps)
+  if (world <= 8 && env_int("LRQ_FUSED_REMAP", 1)) {
+    void* alt = nullptr;
+    if (cudaMalloc(&alt, s->state_bytes) == cudaSuccess) {
+      s->bufs[0] = s->amps;
+      s->bufs[1] = alt;
+    } else {
+      cudaGetLastError();
+    }
   }
   *out = s;
   return LRQ_OK;
@@ -1000,6 +1086,95 @@ int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, co
     return fail(LRQ_ERUNTIME, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
   }
   *out = s;
+  return LRQ_OK;
+}
+
+int lrq_ipc_handles(lrq_state* s, void* out, size_t cap) {
+  if (!s || !out) return fail(LRQ_EVALIDATION, "null argument");
+  if (cap < 2 * sizeof(cudaIpcMemHandle_t)) return fail(LRQ_EVALIDATION, "handle buffer too small");
+  memset(out, 0, 2 * sizeof(cudaIpcMemHandle_t));
+  if (!s->bufs[1]) return LRQ_OK;  // no second buffer: zero handles, fused remap stays off
+  DeviceGuard guard(s->device);
+  cudaIpcMemHandle_t h[2];
+  CUDA_TRY(cudaIpcGetMemHandle(&h[0], s->bufs[0]));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[1], s->bufs[1]));
+  memcpy(out, h, sizeof h);
+  return LRQ_OK;
+}
+
+// peer writes of the fused-remap self-test: rank writes (rank + 1) at the head
+// of its block in every rank's second buffer
+__global__ void fused_probe_kernel(void* const* dst, int world, int rank, size_t block_bytes) {
+  const int b = threadIdx.x;
+  if (b < world) *reinterpret_cast<double*>((char*)dst[b] + (size_t)rank * block_bytes) = (double)(rank + 1);
+}
+
+int lrq_fused_setup(lrq_state* s, const void* all_handles, int* enabled) {
+  if (!s || !all_handles || !enabled) return fail(LRQ_EVALIDATION, "null argument");
+  *enabled = 0;
+  if (s->world < 2 || s->group) return fail(LRQ_EVALIDATION, "lrq_fused_setup is for NCCL ranks");
+  DeviceGuard guard(s->device);
+  const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(all_handles);
+  static const cudaIpcMemHandle_t zero = {};
+  bool ok = s->bufs[1] != nullptr;
+  for (int b = 0; b < s->world && ok; ++b) {
+    for (int i = 0; i < 2 && ok; ++i) {
+      if (b == s->rank) {
+        s->peer[i][b] = s->bufs[i];
+        continue;
+      }
+      if (!memcmp(&h[2 * b + i], &zero, sizeof zero)) {
+        ok = false;
+        break;
+      }
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, h[2 * b + i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+        break;
+      }
+      s->ipc_open.push_back(p);
+      s->peer[i][b] = p;
+    }
+  }
+  // collective self-test of the peer stores (every rank takes part even if
+  // its own mapping failed, so the collectives stay matched)
+  const size_t block = (size_t)s->pbytes << (s->n - s->g);
+  void** dptr = nullptr;
+  double* dv = nullptr;
+  CUDA_TRY(cudaMalloc(&dptr, sizeof(void*) * 8));
+  CUDA_TRY(cudaMalloc(&dv, sizeof(double) * 8));
+  std::vector<void*> dst(8, nullptr);
+  const int nxt = 1 - s->cur;  // probe the buffer that does not hold the state
+  for (int b = 0; b < s->world; ++b) dst[b] = ok ? s->peer[nxt][b] : nullptr;
+  CUDA_TRY(cudaMemcpyAsync(dptr, dst.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice, s->stream));
+  if (ok) {
+    fused_probe_kernel<<<1, 32, 0, s->stream>>>(dptr, s->world, s->rank, block);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  NCCL_TRY(nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));  // barrier
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  float good = 1.0f;
+  if (ok) {
+    for (int b = 0; b < s->world; ++b) {
+      double v = 0.0;
+      CUDA_TRY(cudaMemcpy(&v, (char*)s->bufs[nxt] + (size_t)b * block, sizeof v, cudaMemcpyDeviceToHost));
+      if (v != (double)(b + 1)) good = 0.0f;
+    }
+  } else {
+    good = 0.0f;
+  }
+  // enabled only if every rank passed: minimum over ranks
+  float* dgood = reinterpret_cast<float*>(dv);
+  CUDA_TRY(cudaMemcpy(dgood, &good, sizeof good, cudaMemcpyHostToDevice));
+  NCCL_TRY(nccl().AllReduce(dgood, dgood, 1, ncclFloat, ncclMin, s->comm, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  CUDA_TRY(cudaMemcpy(&good, dgood, sizeof good, cudaMemcpyDeviceToHost));
+  cudaFree(dptr);
+  cudaFree(dv);
+  s->fused = good == 1.0f;
+  *enabled = s->fused ? 1 : 0;
   return LRQ_OK;
 }
 

@@ -312,7 +312,7 @@ inline Plan make_dist_plan(int n_loc, int g, int pair, int p) {
     if (k > 0) z.target1 = lmask;
     z.perm = perm;
     P.sweeps.push_back(z);
-    for (int o = 0; o < Z; ++o) {
+    for (int o = Z - 1; o >= 0; --o) {  // group A last: its contiguous tiles can carry the remap
       PlanSweep m = make_sweep(o, SK_M, k, -1, -1, false);
       m.perm = perm;
       P.sweeps.push_back(m);

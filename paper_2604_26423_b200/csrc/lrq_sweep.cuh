@@ -143,6 +143,13 @@ struct SweepParams {
   double* red_pE;
   double* red_minE;
   unsigned long long* red_arg;
+  // fused remap (distributed plans, group-A M sweep before a remap): the tiles
+  // of block b (top g local bits; 2^rbits tiles each) are stored straight
+  // into rdst[b], rank b's next state buffer at this rank's block (peer
+  // memory over NVLink) instead of in place
+  int remap;
+  int rbits;
+  void* rdst[8];
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }

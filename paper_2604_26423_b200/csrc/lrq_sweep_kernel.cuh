@@ -379,7 +379,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     if constexpr (STORE) {
       constexpr int LO = prog_store_lo(GK, PAIR, SK);
       const int eb = S::ebase(t, LO);
-      U* g = gamps + baseU + S::gunit(eb, qU);
+      U* gbase = gamps + baseU;
+      if constexpr (GK == GK_A && SK == SK_M) {
+        if (P.remap)  // group-A tiles are contiguous: the whole tile goes to one rank
+          gbase = reinterpret_cast<U*>(P.rdst[tid >> P.rbits]) + ((uint64_t)(tid & ((1ll << P.rbits) - 1)) << kUnitBits);
+      }
+      U* g = gbase + S::gunit(eb, qU);
       const int sh = S::gshift(LO, qU);
 #pragma unroll
       for (int j = 0; j < 16; ++j) st_unit(g + ((uint64_t)j << sh), c.r[j]);

@@ -131,6 +131,20 @@ def drain_dist_pool() -> None:
         dev.close()
 
 
+def enable_fused_remap(dev: _native.DeviceState, group=None) -> bool:
+    """Collective: exchange the ranks' state-buffer handles and map them so
+    the sweep before each remap stores straight into peer memory
+    (lrq_fused_setup; falls back to the NCCL remap on every rank if any
+    rank cannot map or verify its peers)."""
+    import torch.distributed as dist
+
+    mine = dev.ipc_handles()
+    world = dist.get_world_size(group)
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    return dev.fused_setup(b"".join(allh))
+
+
 def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Precision.FP32, group=None,
                             device: int | None = None, memory_budget: int | None = None) -> DistStateVector:
     """Collective run of an LR-QAOA circuit over all ranks of `group`."""
@@ -151,6 +165,7 @@ def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Pre
         dist.broadcast_object_list(box, src=0, group=group)
         dev = _native.DeviceState.create_dist(n, precision.bytes_per_amplitude, dev_index, rank, world, box[0],
                                               int(memory_budget or 0))
+        enable_fused_remap(dev, group)
     cost = getattr(circuit, "cost_weights", None)
     dev.set_cost(cost if cost is not None else np.zeros(n * (n - 1) // 2))
     dev.run(layers.phase, layers.mixer)

@@ -54,6 +54,7 @@ LAUNCH_KINDS = {
     "Q": "reduce",        # read-only final pass
     "N": "search",
     "T": "remap",         # block-transpose exchange of the global qubits
+    "Y": "remap (fused)",  # the preceding sweep stored into the peers' buffers; barrier
     "X": "flip",          # deferred global X: index reversal + mirror exchange
     "S": "small",
     "Z": "finalize",
@@ -326,7 +327,7 @@ def _rows_from_timings(per_shard: list[tuple[list, str]], nq: int, G: int) -> li
     rows = []
     for i, k in enumerate(kinds):
         ms = max(t[0][i] for t in per_shard) / 1e3
-        if k == "T":
+        if k in "TY":
             rows.append(GateTiming(i, k, 0.0, ms, (G - 1) << (nq - g)))
         elif k == "X":
             rows.append(GateTiming(i, k, 0.0, ms, (1 << nq) if G > 1 else 0))

@@ -142,3 +142,20 @@ def test_larger_sharded_runs_match_dense(n, G, p, prec, dbeta):
         dense.release()
     finally:
         sv.release()
+
+
+@pytest.mark.parametrize("n,G,p,prec", [(16, 2, 3, "fp64"), (18, 4, 2, "fp32"), (26, 8, 3, "fp64")])
+def test_fused_remap_equals_swap_remap(monkeypatch, n, G, p, prec):
+    """The fused remap (the group-A sweep stores each block into its owner's
+    next buffer) moves exactly what the separate block swap moves: the
+    amplitudes are bitwise identical."""
+    circ = L.build_circuit(L.generate_instance(n, 6), L.LrQaoaParams(p=p, delta_beta=0.9))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("LRQ_FUSED_REMAP", flag)
+        sv, rec = L.run_circuit_sharded(circ, L.plan_for_shard_count(n, G), prec)
+        out[flag] = (sv.amps.copy(), None, [g.kind for g in rec.gates])
+        sv.release()
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    assert "Y" in out["1"][2] and "Y" not in out["0"][2]
+    assert [k.replace("Y", "T") for k in out["1"][2]] == out["0"][2]
