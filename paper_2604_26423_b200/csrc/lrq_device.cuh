@@ -209,9 +209,11 @@ __device__ __forceinline__ void st_unit(double2* p, double2 v) { __stcs(p, v); }
 
 // |a|^2 in float64 with the reference's rounding: re*re and im*im each rounded,
 // then added (engine.py:94-96) — no FMA contraction.
+// complex64: both squares are exact in fp64 (24-bit mantissas), so one
+// rounding of x^2 + y^2 (the fma) equals the reference's float64 re^2 + im^2
 __device__ __forceinline__ double prob(float2 a) {
   double x = (double)a.x, y = (double)a.y;
-  return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+  return __fma_rn(x, x, __dmul_rn(y, y));
 }
 __device__ __forceinline__ double prob(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
 

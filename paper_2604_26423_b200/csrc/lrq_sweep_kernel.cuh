@@ -324,15 +324,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
     c.base = baseU << PAIR;
     c.tid = tid;
-    double* hbJ = hB + (par * 2 + 0) * 16;
-    double* hbW = hB + (par * 2 + 1) * 16;
-    if (HAS_PHASE) S::block_consts(Jm, Jx, P.J.cst, n, q0, c.base, 0, hbJ, &EBB[par * 2 + 0], t);
-    if (usesW) S::block_consts(Wm, Wx, P.W.cst, n, q0, c.base, 2, hbW, &EBB[par * 2 + 1], t);
-    __syncthreads();
-    c.hbJ = hbJ;
-    c.hbW = hbW;
-    c.ebbJ = EBB[par * 2 + 0];
-    c.ebbW = EBB[par * 2 + 1];
 
     if constexpr (AMPS && !INIT) {
       constexpr int LO = prog_lo(GK, PAIR, SK, 0);
@@ -359,7 +350,22 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
           }
         }
       }
-      if (!HAS_PHASE && !(P.scale_re == 1.0 && P.scale_im == 0.0)) {
+    }
+
+    // the tile's block constants (serial fp64 chains on two warps) are
+    // computed while its loads are in flight; hB[par] was last read two
+    // tiles ago, before the previous tile's barrier
+    double* hbJ = hB + (par * 2 + 0) * 16;
+    double* hbW = hB + (par * 2 + 1) * 16;
+    if (HAS_PHASE) S::block_consts(Jm, Jx, P.J.cst, n, q0, c.base, 0, hbJ, &EBB[par * 2 + 0], t);
+    if (usesW) S::block_consts(Wm, Wx, P.W.cst, n, q0, c.base, 2, hbW, &EBB[par * 2 + 1], t);
+    __syncthreads();
+    c.hbJ = hbJ;
+    c.hbW = hbW;
+    c.ebbJ = EBB[par * 2 + 0];
+    c.ebbW = EBB[par * 2 + 1];
+    if constexpr (AMPS && !INIT && !HAS_PHASE) {
+      if (!(P.scale_re == 1.0 && P.scale_im == 0.0)) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           A x = amp_get(c.r, v);
