@@ -458,6 +458,9 @@ int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
     return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
   sp.has_tmap = 1;
   sp.nstages = 3;
+  // measured: +1-2 % on H groups, -35 % on H4 (its 512-row tensor prefetch
+  // competes with the ring's own loads and stores)
+  sp.wd_prefetch = env_int("LRQ_WD_PREFETCH", gk == GK_H ? 1 : 0);
   const size_t smem = wd_smem_bytes(sp.n, 3, sk == SK_F || sk == SK_P);
   if (smem > 227 * 1024) return fail(LRQ_ERUNTIME, "internal: warp-decoupled sweep needs too much shared memory");
   const int sms = sm_count(s->device);

@@ -150,6 +150,7 @@ struct SweepParams {
   int remap;
   int rbits;
   void* rdst[8];
+  int wd_prefetch;  // warp-decoupled sweeps: L2 prefetch of the next tile at each refill
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -266,21 +267,31 @@ struct SweepCtx {
   __device__ static void block_consts(const double* M, const double* X, double cst, int n, int q0, uint64_t base,
                                       int w0, double* hb, double* ebb, int tl) {
     const int warp = tl >> 5, lane = tl & 31;  // tl: thread index within the 256-thread team
+    // the block bits are [MA, q0) and [q0 + KA - MA, n), visited in ascending
+    // order (the same sums as a full j loop that skips the tile bits, without
+    // a branch per bit)
+    const int lo_end = q0 < n ? q0 : n, hi_beg = q0 + KA - MA > MA ? q0 + KA - MA : MA;
     if (warp == w0) {
       if (lane < KA) {
         const int gi = gpos(lane, q0);
+        const double* Mi = M + gi * n;
         double acc = X[gi];
-        for (int j = 0; j < n; ++j)
-          if (blockbit(j, q0)) acc += M[gi * n + j] * spin(base, j);
+#pragma unroll 4
+        for (int j = MA; j < lo_end; ++j) acc += Mi[j] * spin(base, j);
+#pragma unroll 4
+        for (int j = hi_beg; j < n; ++j) acc += Mi[j] * spin(base, j);
         hb[lane] = acc;
       }
     } else if (warp == w0 + 1) {
       double term = 0.0;
       for (int j = lane; j < n; j += 32) {
         if (!blockbit(j, q0)) continue;
+        const double* Mj = M + j * n;
         double f = 0.0;
-        for (int l = 0; l < n; ++l)
-          if (blockbit(l, q0)) f += M[j * n + l] * spin(base, l);
+#pragma unroll 4
+        for (int l = MA; l < lo_end; ++l) f += Mj[l] * spin(base, l);
+#pragma unroll 4
+        for (int l = hi_beg; l < n; ++l) f += Mj[l] * spin(base, l);
         term += spin(base, j) * (X[j] + 0.5 * f);
       }
       for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);

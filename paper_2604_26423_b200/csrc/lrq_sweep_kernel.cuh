@@ -343,10 +343,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
           // one TMA tensor prefetch covers all 2^(12-MU) strided runs of the tile
           if (P.has_tmap && nxt < P.num_tiles) {
             const int c1 = (int)((uint64_t)nxt & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)nxt >> bl);
-            asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
-                             reinterpret_cast<uint64_t>(&P.tmap)),
-                         "r"(0), "r"(c1), "r"(0), "r"(0), "r"(c4)
-                         : "memory");
+            tma_prefetch_5d(&P.tmap, 0, 0, c1, 0, c4);
           }
         }
       }
