@@ -181,3 +181,16 @@ def test_dist_plan_validation():
     kinds = [s["kind"] for s in plan["sweeps"]]
     assert kinds[0] == "P" and kinds[-1] == "Q"
     assert sum(r for _, r, _ in plan["dist"]) == 4  # 3 layer remaps + 1 restoring
+
+
+@pytest.mark.parametrize("n,g,B,p", [(32, 3, 8, 3), (34, 3, 16, 3), (30, 1, 8, 2), (29, 2, 16, 4), (36, 3, 16, 3)])
+def test_dist_plan_remap_follows_group_a_mixer(n, g, B, p):
+    """The fused remap redirects the stores of the sweep before a remap; that
+    needs a group-A (contiguous-tile) mixer-only sweep there.  Every layer
+    remap has one; the restoring remap of an odd p follows the last mixer
+    sweep of another group and runs as an exchange."""
+    plan = json.loads(_native.describe_dist_plan(n, g, B, p))
+    before = [(sw["kind"], plan["groups"][sw["group"]]["kind"])
+              for sw, (_, remap_after, _) in zip(plan["sweeps"], plan["dist"]) if remap_after]
+    assert len(before) == p + (p % 2)
+    assert all(b == ("M", "A") for b in before[:p])
