@@ -457,7 +457,7 @@ def run_ours_dist(args, rank, world, local_rank, dist):
                                f"{'complex64' if B == 8 else 'complex128'}, one state over {world} B200s "
                                f"(2^{nl} amplitudes per GPU)",
                    "n": n, "n_local": nl, "p": p, "precision": args.precision, "shots": args.shots,
-                   "state_bytes": B << n, "parallelism": f"global-qubit sharding x{world} (NCCL remap per layer)",
+                   "state_bytes": B << n, "parallelism": f"global-qubit sharding x{world} (one remap per layer: fused peer stores, NCCL fallback)",
                    "l2": "shard >> L2 (126 MB); no flush needed"},
         "e2e": {"value": amp_updates / e2e_s_max, "unit": "amp-updates/s",
                 "h2d_bytes_per_step": int(lay.phase.nbytes + lay.mixer.nbytes + w.nbytes + args.shots * 8),
