@@ -1,0 +1,53 @@
+"""GPU parity at BASELINE.json's full single-GPU sizes, through properties
+that do not need the (infeasible) CPU oracle at 2^32-2^33 amplitudes:
+
+* configs[2] (n=32, p=10; the bench workload, 32 GiB in complex64) and the
+  1-GPU point of configs[3] (n=33, p=3; 128 GiB in complex128): the
+  complex64 run against the complex128 run of the same circuit;
+* norm (sum of probabilities from the fused final pass) to 1e-12 in
+  complex128 and 1e-5 in complex64;
+* exact r agreeing to the complex64 tolerance (1e-5 relative);
+* the max cut found by the fused final pass equals C* of the exhaustive GPU
+  search, and is the same state in both precisions;
+* the sampled r within 4 standard errors of the exact r.
+"""
+import math
+
+import pytest
+
+import paper_2604_26423_b200 as L
+from paper_2604_26423_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+BUDGET = 1 << 40
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _engine():
+    from paper_2604_26423_b200.build import build
+    build()
+    assert _native.device_count() >= 1, "GPU tests need a CUDA device"
+
+
+@pytest.mark.parametrize("n,p", [(32, 10), (33, 3)])
+def test_full_size_complex64_against_complex128(n, p):
+    inst = L.solve_instance(L.generate_instance(n, 1), limit=n)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=p))
+    out = {}
+    for prec in ("fp32", "fp64"):
+        sv = L.run_circuit(circ, prec, BUDGET)
+        red = sv.device_state.reduce()
+        shots = L.sample(sv, 4000, rng_seed=1) if prec == "fp32" else None
+        out[prec] = (L.exact_expected_r(sv, inst), red, shots)
+        sv.release()
+        _native.drain_pool()
+    (r32, red32, shots), (r64, red64, _) = out["fp32"], out["fp64"]
+    assert abs(red64.sum_p - 1.0) < 1e-12
+    assert abs(red32.sum_p - 1.0) < 1e-5
+    assert r32 == pytest.approx(r64, rel=1e-5)
+    assert red32.argmax_cut == red64.argmax_cut
+    assert float(L.cut_values(inst, [red64.argmax_cut])[0]) == inst.optimal_cut.value
+    ratios = L.shot_ratios(inst, shots)
+    se = ratios.std() / math.sqrt(len(ratios))
+    assert abs(ratios.mean() - r64) < 4 * se
