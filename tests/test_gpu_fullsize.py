@@ -51,3 +51,30 @@ def test_full_size_complex64_against_complex128(n, p):
     ratios = L.shot_ratios(inst, shots)
     se = ratios.std() / math.sqrt(len(ratios))
     assert abs(ratios.mean() - r64) < 4 * se
+
+
+def test_full_size_distributed_plan_matches_dense():
+    """The distributed plan (rank-local phase fields, a fused remap per
+    layer, the rank-partitioned reductions and sampler) at the bench size:
+    n=32 on 8 in-process shards of 2^29 amplitudes against the dense run."""
+    n, G, p = 32, 8, 4
+    inst = L.solve_instance(L.generate_instance(n, 1), limit=n)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=p))
+    sv, rec = L.run_circuit_sharded(circ, L.plan_for_shard_count(n, G), "fp32", BUDGET)
+    try:
+        assert isinstance(sv, L.ShardedStateVector)
+        assert "Y" in [g.kind for g in rec.gates]  # the remaps ran fused
+        r_sh = L.exact_expected_r(sv, inst)
+        shots_sh = L.sample(sv, 2000, rng_seed=2)
+    finally:
+        sv.release()
+    dense = L.run_circuit(circ, "fp32", BUDGET)
+    r_de = L.exact_expected_r(dense, inst)
+    shots_de = L.sample(dense, 2000, rng_seed=2)
+    dense.release()
+    assert r_sh == pytest.approx(r_de, rel=1e-5)
+    # at 2^32 outcomes complex64 rounding moves CDF boundaries across many
+    # states, so shots need not coincide; both sample the same distribution
+    for shots in (shots_sh, shots_de):
+        ratios = L.shot_ratios(inst, shots)
+        assert abs(ratios.mean() - r_de) < 4 * ratios.std() / math.sqrt(len(ratios))
