@@ -813,7 +813,8 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
-    const bool fuse = w.remap_after && fused && gr.kind == GK_A && w.kind == SK_M;
+    // (a tile must lie inside one destination block: n_loc - g >= tile bits)
+    const bool fuse = w.remap_after && fused && gr.kind == GK_A && w.kind == SK_M && nl - g >= P.KA;
     if (fuse) {
       // the sweep stores block b of its output into rank b's next buffer at
       // this rank's block: the remap rides on the sweep's own stores
@@ -1033,7 +1034,7 @@ int create_rank_state(int n_total, int pbytes, int device, int rank, int world, 
   while ((1 << g) < world) ++g;
   const int nl = n_total - g, KA = tile_amp_bits(pbytes);
   if (nl <= KA) return fail(LRQ_EVALIDATION, "distributed engine needs n - log2(world) > " + std::to_string(KA));
-  if (plan_groups(nl, pair_of(pbytes)).back().ntargets < g)
+  if (make_dist_plan(nl, g, pair_of(pbytes), 1).groups.back().ntargets < g)
     return fail(LRQ_EVALIDATION, "last qubit group smaller than log2(world); choose another n");
   lrq_state* s = nullptr;
   int rc = lrq_create(nl, pbytes, device, memory_budget, &s);

@@ -299,6 +299,23 @@ inline Plan make_dist_plan(int n_loc, int g, int pair, int p) {
   P.groups = plan_groups(n_loc, pair);
   const int S = (int)P.groups.size();
   const int Z = S - 1;
+  // the remap swaps the top g local qubits L' into the rank bits, so all of
+  // L' must be targets of Z.  A short last group (fewer than g targets) takes
+  // the missing ones from the top of the group below: its tile slid down to
+  // the top of the range and already holds them as non-target bits.
+  if (S >= 2 && P.groups[Z].ntargets < g) {
+    PlanGroup& z = P.groups[Z];
+    PlanGroup& y = P.groups[Z - 1];
+    const int lo = n_loc - g, hi = n_loc - z.ntargets;  // qubits [lo, hi) move from y to z
+    for (int i = 0; i < P.KA; ++i) {
+      const int gy = i < y.m ? i : y.q0 + (i - y.m);
+      if (gy >= lo && gy < hi && ((y.tmask >> i) & 1u)) y.tmask &= ~(1u << i);
+      const int gz = i < z.m ? i : z.q0 + (i - z.m);
+      if (i >= z.m && gz >= lo && gz < hi) z.tmask |= 1u << i;
+    }
+    y.ntargets -= hi - lo;
+    z.ntargets += hi - lo;
+  }
   const PlanGroup& gz = P.groups[Z];
   // tile bits of group Z holding the top g local qubits L'
   unsigned lmask = 0;

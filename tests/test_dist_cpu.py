@@ -133,7 +133,7 @@ def _lib():
     build()
 
 
-@pytest.mark.parametrize("world,n,p", [(2, 16, 3), (4, 17, 2), (2, 17, 4)])
+@pytest.mark.parametrize("world,n,p", [(2, 16, 3), (4, 17, 2), (2, 17, 4), (4, 15, 2), (8, 17, 3)])
 def test_distributed_plan_emulation_matches_oracle(world, n, p):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
@@ -194,3 +194,25 @@ def test_dist_plan_remap_follows_group_a_mixer(n, g, B, p):
               for sw, (_, remap_after, _) in zip(plan["sweeps"], plan["dist"]) if remap_after]
     assert len(before) == p + (p % 2)
     assert all(b == ("M", "A") for b in before[:p])
+
+
+@pytest.mark.parametrize("B", [8, 16])
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_dist_plan_groups_partition_the_local_qubits(g, B):
+    """Every n with n_local above the tile is plannable: the groups' mixer
+    targets partition the local qubits, and the last group holds the top g
+    (the qubits a remap swaps out), taking them from the group below when
+    it is short."""
+    KA = 13 if B == 8 else 12
+    for n in range(KA + g + 1, 40):
+        plan = json.loads(_native.describe_dist_plan(n, g, B, 2))
+        nl = n - g
+        seen = []
+        for grp in plan["groups"]:
+            for i in range(KA):
+                if (grp["tmask"] >> i) & 1:
+                    seen.append(i if i < grp["m"] else grp["q0"] + i - grp["m"])
+        assert sorted(seen) == list(range(nl)), (n, g, B)
+        last = plan["groups"][-1]
+        top = {last["q0"] + i - last["m"] for i in range(last["m"], KA) if (last["tmask"] >> i) & 1}
+        assert set(range(nl - g, nl)) <= top

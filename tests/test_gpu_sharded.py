@@ -37,6 +37,11 @@ def _engine():
     (18, 8, 2, "fp64", 0.2),
     (18, 4, 4, "fp32", 0.2),
     (19, 2, 5, "fp32", 1.0),
+    # short last group: the top local qubits come from the group below
+    (17, 8, 3, "fp64", 0.9),
+    (17, 8, 3, "fp64", 0.2),
+    (15, 4, 2, "fp64", 0.2),
+    (17, 8, 2, "fp32", 0.2),
 ])
 def test_sharded_matches_oracle_and_dense(n, G, p, prec, dbeta):
     inst = L.solve_instance(L.generate_instance(n, 3))
