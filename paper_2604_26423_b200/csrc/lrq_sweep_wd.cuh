@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
     for (int b = 0; b < 32; ++b) st[W::nat(wq, lane, b)] = r[b];
     fence_proxy_async();
     team_sync_n(1 + team, kWdWarps * 32);
-    if (wq == kWdWarps - 1 && lane == 0) {  // warp 0 computes the next tile's fields
+    if (wq == kWdWarps - 1 && lane == 0) {  // the last warp stores (warp 0 computes the next tile's fields)
       const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
       tma_store_5d(&P.tmap, st, 0, 0, c1, 0, c4);
       bulk_commit();
