@@ -160,6 +160,9 @@ def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Pre
     layers = lower_circuit(circuit)
     dev_index = _native.default_device() if device is None else int(device)
     dev = _DIST_POOL.pop((n, precision.bytes_per_amplitude, dev_index, rank, world, id(group)), None)
+    if dev is None and world == 1:
+        # one rank: the single-GPU engine (same methods, no communicator)
+        dev = _native.DeviceState(n, precision.bytes_per_amplitude, dev_index, int(memory_budget or 0))
     if dev is None:
         box = [_native.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0, group=group)

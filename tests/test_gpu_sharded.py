@@ -164,3 +164,35 @@ def test_fused_remap_equals_swap_remap(monkeypatch, n, G, p, prec):
     np.testing.assert_array_equal(out["1"][0], out["0"][0])
     assert "Y" in out["1"][2] and "Y" not in out["0"][2]
     assert [k.replace("Y", "T") for k in out["1"][2]] == out["0"][2]
+
+
+def test_distributed_api_with_one_rank_runs_the_single_gpu_engine():
+    """run_circuit_distributed under a one-rank process group (torchrun
+    --nproc-per-node 1) is the single-GPU engine: results equal run_circuit's."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2604_26423_b200.distributed import drain_dist_pool, run_circuit_distributed
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        inst = L.solve_instance(L.generate_instance(16, 5))
+        circ = L.build_circuit(inst, L.LrQaoaParams(p=3))
+        sv = run_circuit_distributed(circ, "fp64")
+        r = sv.exact_expected_r(inst)
+        shots = sv.sample(500, 4)
+        amps = sv.gather_amps()
+        sv.release()
+        dense = L.run_circuit(circ, "fp64")
+        assert r == L.exact_expected_r(dense, inst)
+        np.testing.assert_array_equal(shots.indices, L.sample(dense, 500, rng_seed=4).indices)
+        np.testing.assert_array_equal(amps, dense.amps)
+        dense.release()
+        drain_dist_pool()
+    finally:
+        dist.destroy_process_group()
