@@ -153,6 +153,33 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def pattern_ceilings():
+    """Measured copy ceilings of the sweep tile shapes (compute-free TMA copy)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "pattern_ceilings.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+def pattern_fraction(n, B, p, sw):
+    """Sweep time at the measured copy ceiling of each sweep's tile pattern
+    (contiguous A tiles, strided H / H4 runs) over the measured sweep time."""
+    ceil = pattern_ceilings()
+    key = "c64" if B == 8 else "c128"
+    if not ceil or key not in ceil:
+        return None
+    from paper_2604_26423_b200 import _native
+    plan = json.loads(_native.describe_plan(n, B, p))
+    kinds = [plan["groups"][s["group"]]["kind"] for s in plan["sweeps"]]
+    if not kinds or len(sw) % len(kinds):
+        return None
+    ideal = sum((1 if k == "P" else 2) * (B << n) / (ceil[key][kinds[i % len(kinds)]] * 1e9)
+                for i, (_, k) in enumerate(sw))
+    return {"frac": ideal / (sum(m for m, _ in sw) * 1e-3), "ceilings_GBps": ceil[key],
+            "source": "profiles/pattern_ceilings.json"}
+
+
 def profiled_traffic():
     """dram read+write bytes per sweep launch from the committed ncu capture."""
     try:
@@ -338,7 +365,8 @@ def run_ours(args, rank, world, local_rank, dist):
                      "frac": per_launch_achieved / peak, "peak_source": peak_kind,
                      "traffic": traffic.get(f"n{n}_{args.precision}") if traffic else None,
                      "kernel": "sweep_kernel", "bytes_per_launch": 2 * (B << n),
-                     "launch_ms_avg": sweep_time_s * 1e3 / max(1, len(sw))},
+                     "launch_ms_avg": sweep_time_s * 1e3 / max(1, len(sw)),
+                     "vs_pattern_ceiling": pattern_fraction(n, B, p, sw)},
         "sweeps_per_step": len(sw) // args.steps,
         "sweep_ms": {k: round(statistics.mean(m for m, kk in sw if kk == k), 3) for k in sorted(set(kinds_all)) if k in "PMFR"},
         "gpu_launches": launches_per_step * args.steps,
