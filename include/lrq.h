@@ -31,7 +31,7 @@ extern "C" {
 #define LRQ_ECAPACITY 3
 #define LRQ_ERUNTIME 4
 
-#define LRQ_ABI_VERSION 1
+#define LRQ_ABI_VERSION 2
 
 typedef struct lrq_state lrq_state; /* one state vector (or one rank's shard) in HBM */
 
@@ -40,6 +40,7 @@ typedef struct lrq_reduction {
   double sum_p_cut;    /* sum_z |a_z|^2 C(z)  -> exact r = sum_p_cut / C*  */
   double min_energy;   /* min_z E_w(z) over z with top bit 0 (spin form)   */
   uint64_t argmax_cut; /* lowest-index z attaining it (= argmax C)         */
+  double max_energy;   /* max_z E_w(z) (= W - 2 min C: the minimum cut)     */
 } lrq_reduction;
 
 /* library / device ------------------------------------------------------- */
@@ -112,6 +113,17 @@ int lrq_reduce(lrq_state *s, lrq_reduction *out);
  * current state with the current cost (zero cost if none was set).         */
 int lrq_recompute(lrq_state *s);
 
+/* p-weighted histogram of the cost energy E_w(z) over `bins` equal bins of
+ * [lo, hi) (values outside clamp to the end bins), filled by the fused final
+ * pass of the next lrq_run / lrq_recompute (bins = 0: off, the default; on,
+ * the reducing pass adds one shared-memory integer atomic per amplitude).
+ * raw[b] = sum over z in bin b of round(|a_z|^2 2^60): integer sums, so the
+ * result is identical in any order and on any number of ranks (collective:
+ * summed over ranks).  Exact distribution of C = (W - E)/2 for the
+ * chi-square test of sampled shots.                          */
+int lrq_set_histogram(lrq_state *s, int bins, double lo, double hi);
+int lrq_get_histogram(lrq_state *s, uint64_t *raw);
+
 /* inverse-CDF sampling (engine.py:254-273) with caller-supplied uniforms
  * (the reference draws them from Philox("shots", 0) on the host).           */
 int lrq_sample(lrq_state *s, const double *u, int64_t shots, uint64_t *idx_out);
@@ -125,6 +137,25 @@ int lrq_store_amps(lrq_state *s, uint64_t start, uint64_t count, const void *hos
  * contiguous range [start, start+count).                                    */
 int lrq_cut_values(int num_qubits, const double *w, const uint64_t *z, uint64_t start, int64_t count,
                    double *out, int device);
+
+/* spin-form cut values C = W/2 - s^T A s / 4 of the contiguous range
+ * [start, start+count) — cut_values_range (problem.py:158-171); half_total =
+ * 0.5 * WmcInstance.total_weight().  Equal to lrq_cut_values to ~1e-15.     */
+int lrq_cut_values_spin(int num_qubits, const double *w, double half_total, uint64_t start, int64_t count,
+                        double *out, int device);
+
+/* numerator of expected_r_from_probs (engine.py:214-226) for an explicit
+ * float64 distribution of 2^n entries: chunk_sums[c] = sum over the c-th 2^16
+ * block of p_z * C_spin(z) (2^n / 2^16 outputs, or 1 for n < 16); the caller
+ * adds them in order.                                                       */
+int lrq_expected_cut(int num_qubits, const double *w, double half_total, const double *probs, uint64_t count,
+                     double *chunk_sums, int device);
+
+/* draw_indices (engine.py:254-263) over an explicit float64 distribution:
+ * first index whose normalised cumulative probability exceeds u[i], clamped
+ * to count-1.  Zero total mass -> 2 ("statevector has zero norm").         */
+int lrq_draw_indices(const double *probs, uint64_t count, const double *u, int64_t shots, uint64_t *idx_out,
+                     int device);
 
 /* exhaustive max cut (optimal_cut_bruteforce, problem.py:174-211) on the
  * device: lowest-index argmax of C; value re-evaluated bit-exactly.         */
@@ -141,16 +172,36 @@ int lrq_create_dist(int num_qubits, int precision_bytes, int device, int rank, i
                     uint64_t memory_budget, lrq_state **out);
 int lrq_dist_info(lrq_state *s, int *n_local, int *rank, int *world);
 
-/* Fused remap over peer memory (NVLink): each rank keeps two state buffers and
- * the sweep before a remap stores every block straight into its owner rank's
- * next buffer, so the all-to-all rides on the sweep.  Collective setup: every
- * rank exports its two buffers (lrq_ipc_handles, 128 bytes), the host gathers
- * them in rank order (world * 128 bytes) and every rank calls lrq_fused_setup,
- * which maps the peers' buffers and runs a peer-store self-test; *enabled = 1
- * on all ranks or on none (then the NCCL remap is used).  In-process shard
- * groups use the members' buffers directly.  LRQ_FUSED_REMAP=0 disables.   */
+/* Remap transports over peer memory (NVLink).  Collective setup: every rank
+ * exports its buffers (lrq_ipc_handles, LRQ_IPC_HANDLE_BYTES bytes), the host
+ * gathers them in rank order (world * LRQ_IPC_HANDLE_BYTES bytes) and every
+ * rank calls lrq_fused_setup, which maps the peers' buffers and runs a
+ * peer-store self-test.  *enabled (the same on all ranks):
+ *   1  fused remap: every rank holds a spare state buffer, and the sweep
+ *      before a remap stores every block straight into its owner's spare;
+ *   2  pipelined remap over peer memory: the sweep before a remap runs block
+ *      by block and each finished block is swapped in place with its owner
+ *      (XOR schedule, no second buffer: the case at the HBM limit);
+ *   0  NCCL send/recv remap (pipelined the same way, through a staging chunk).
+ * The spare buffer is taken only if it fits with 2 GiB to spare.  In-process
+ * shard groups use the members' buffers directly.  LRQ_FUSED_REMAP=0 disables
+ * the fused form, LRQ_PIPELINED_REMAP=0 the block pipelining.            */
+#define LRQ_IPC_HANDLE_BYTES 256
 int lrq_ipc_handles(lrq_state *s, void *out, size_t cap);
 int lrq_fused_setup(lrq_state *s, const void *all_handles, int *enabled);
+
+/* Host-only accounting: device bytes one rank allocates for an n-qubit state
+ * over `world` ranks (world 1: the single-GPU engine) at depth p — the state,
+ * reductions, cost matrices and (NCCL transport) the staging chunk; the
+ * fused remap's optional spare buffer is extra_spare.                      */
+/* Host-only: the remap schedule of `rank` as JSON [[partner, my_block,
+ * their_block, half], ...] — the XOR pairwise steps of the all-to-all block
+ * transpose (mirror < 0) or the one whole-state step with rank `mirror`
+ * (block -1) of the deferred global flip.                                  */
+int lrq_describe_remap(int world, int rank, int mirror, char *buf, size_t cap);
+
+int lrq_describe_memory(int num_qubits, int precision_bytes, int world, int p, uint64_t *state_bytes,
+                        uint64_t *other_bytes, uint64_t *extra_spare);
 
 /* in-process shards — the B200 form of the reference's thread-per-shard
  * engine (run_circuit_sharded / _ShardWorker, sharded.py:200-385): `world`

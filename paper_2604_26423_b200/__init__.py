@@ -22,7 +22,10 @@ from .circuit import (
     lower_circuit,
 )
 from .engine import (
+    CutDistribution,
     Precision,
+    draw_indices,
+    exact_cut_distribution,
     apply_gate,
     apply_h,
     apply_rx,

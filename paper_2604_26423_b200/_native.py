@@ -13,11 +13,11 @@ import threading
 
 import numpy as np
 
-from .errors import CapacityError, StateError, ValidationError
+from .errors import AbortedRunError, CapacityError, StateError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "liblrq.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 _lock = threading.Lock()
@@ -29,7 +29,8 @@ _state_p = ctypes.c_void_p
 
 class Reduction(ctypes.Structure):
     _fields_ = [("sum_p", ctypes.c_double), ("sum_p_cut", ctypes.c_double),
-                ("min_energy", ctypes.c_double), ("argmax_cut", ctypes.c_uint64)]
+                ("min_energy", ctypes.c_double), ("argmax_cut", ctypes.c_uint64),
+                ("max_energy", ctypes.c_double)]
 
 
 _SIGNATURES = {
@@ -54,7 +55,12 @@ _SIGNATURES = {
     "lrq_store_amps": ([_state_p, _c_u64, _c_u64, _p], _c_int),
     "lrq_cut_values": ([_c_int, _p, _p, _c_u64, _c_i64, _p, _c_int], _c_int),
     "lrq_max_cut": ([_c_int, _p, _c_int, ctypes.POINTER(_c_u64), ctypes.POINTER(_c_dbl)], _c_int),
+    "lrq_cut_values_spin": ([_c_int, _p, _c_dbl, _c_u64, _c_i64, _p, _c_int], _c_int),
+    "lrq_expected_cut": ([_c_int, _p, _c_dbl, _p, _c_u64, _p, _c_int], _c_int),
+    "lrq_draw_indices": ([_p, _c_u64, _p, _c_i64, _p, _c_int], _c_int),
     "lrq_set_timing": ([_state_p, _c_int], _c_int),
+    "lrq_set_histogram": ([_state_p, _c_int, _c_dbl, _c_dbl], _c_int),
+    "lrq_get_histogram": ([_state_p, _p], _c_int),
     "lrq_get_timings": ([_state_p, _p, ctypes.c_char_p, _c_int, ctypes.POINTER(_c_int)], _c_int),
     "lrq_stream": ([_state_p, ctypes.POINTER(_p)], _c_int),
     "lrq_synchronize": ([_state_p], _c_int),
@@ -69,7 +75,12 @@ _SIGNATURES = {
     "lrq_dist_info": ([_state_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
     "lrq_describe_dist_plan": ([_c_int, _c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
     "lrq_dist_terms": ([_c_int, _c_int, _c_int, _c_int, _p, _p, _p, ctypes.POINTER(_c_dbl)], _c_int),
+    "lrq_describe_remap": ([_c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
+    "lrq_describe_memory": ([_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_u64), ctypes.POINTER(_c_u64),
+                             ctypes.POINTER(_c_u64)], _c_int),
 }
+
+IPC_HANDLE_BYTES = 256  # LRQ_IPC_HANDLE_BYTES
 
 EXPORTED = tuple(_SIGNATURES)
 
@@ -102,6 +113,8 @@ def check(rc: int) -> None:
         raise ValidationError(msg)
     if rc == 3:
         raise CapacityError(msg)
+    if msg.startswith("aborted run"):  # a collective failed on this or another rank
+        raise AbortedRunError(msg)
     raise StateError(msg)
 
 
@@ -112,9 +125,16 @@ def device_count() -> int:
 
 
 def default_device() -> int:
-    """Device for new states: $LRQ_DEVICE, else 0 (one process per GPU; torchrun
-    launches pin CUDA_VISIBLE_DEVICES or pass LOCAL_RANK explicitly)."""
-    return int(os.environ.get("LRQ_DEVICE", "0"))
+    """Device for new states: $LRQ_DEVICE; else, under a torchrun launch
+    (LOCAL_RANK set), the local rank modulo the visible devices, so one
+    process per GPU lands on its own GPU; else 0."""
+    if os.environ.get("LRQ_DEVICE"):
+        return int(os.environ["LRQ_DEVICE"])
+    lr = os.environ.get("LOCAL_RANK")
+    if lr is not None and int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1"))) > 1:
+        n = device_count()
+        return int(lr) % n if n > 0 else int(lr)
+    return 0
 
 
 def describe_plan(n: int, precision_bytes: int, p: int) -> str:
@@ -145,6 +165,22 @@ def dist_terms(n: int, log2_world: int, rank: int, perm: int, edges: np.ndarray)
     return m, f, float(c.value)
 
 
+def describe_remap(world: int, rank: int, mirror: int = -1) -> list:
+    """The remap schedule of `rank` (host-only, lrq_describe_remap)."""
+    import json
+
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(lib().lrq_describe_remap(world, rank, mirror, buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def describe_memory(n: int, precision_bytes: int, world: int, p: int = 1) -> dict:
+    """Device bytes one rank allocates (host-only accounting, lrq_describe_memory)."""
+    a, b, c = _c_u64(0), _c_u64(0), _c_u64(0)
+    check(lib().lrq_describe_memory(n, precision_bytes, world, p, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return {"state": int(a.value), "other": int(b.value), "spare": int(c.value)}
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     check(lib().lrq_nccl_unique_id(buf, 128))
@@ -153,7 +189,11 @@ def nccl_unique_id() -> bytes:
 
 # One parked lrq_state per (n, precision, device): run_circuit in a loop then
 # reuses the HBM allocation instead of cudaFree/cudaMalloc of the whole state.
+# Only states up to _POOL_MAX_BYTES are parked (a parked 128 GiB state would
+# block every other allocation), and a failed allocation drains the pool and
+# retries once.
 _POOL: dict = {}
+_POOL_MAX_BYTES = 64 << 30
 
 
 def drain_pool() -> None:
@@ -179,7 +219,13 @@ class DeviceState:
             self.set_cost(np.zeros(n * (n - 1) // 2))
             return
         h = _state_p()
-        check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
+        try:
+            check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
+        except CapacityError:
+            if not _POOL:
+                raise
+            drain_pool()
+            check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
         self._h = h
 
     @classmethod
@@ -219,16 +265,17 @@ class DeviceState:
         return self
 
     def ipc_handles(self) -> bytes:
-        buf = ctypes.create_string_buffer(128)
-        check(lib().lrq_ipc_handles(self.handle, buf, 128))
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        check(lib().lrq_ipc_handles(self.handle, buf, IPC_HANDLE_BYTES))
         return buf.raw
 
-    def fused_setup(self, all_handles: bytes) -> bool:
-        """Collective: map the peers' state buffers for the fused remap."""
+    def fused_setup(self, all_handles: bytes) -> int:
+        """Collective: map the peers' buffers; returns the remap transport
+        (1 fused, 2 pipelined over peer memory, 0 NCCL send/recv)."""
         buf = ctypes.create_string_buffer(all_handles, len(all_handles))
         on = _c_int(0)
         check(lib().lrq_fused_setup(self.handle, buf, ctypes.byref(on)))
-        return bool(on.value)
+        return int(on.value)
 
     def close(self, park: bool = True) -> None:
         """Release the state (distributed shards are never parked)."""
@@ -247,7 +294,7 @@ class DeviceState:
         pool already holds one for this shape (or park=False)."""
         if self._h is not None and _lib is not None:
             key = (self.n, self.precision_bytes, self.device)
-            if park and key not in _POOL:
+            if park and key not in _POOL and (self.precision_bytes << self.n) <= _POOL_MAX_BYTES:
                 _POOL[key] = self._h
             else:
                 _lib.lrq_destroy(self._h)
@@ -322,6 +369,17 @@ class DeviceState:
         amps = np.ascontiguousarray(amps, dtype=dt)
         check(lib().lrq_store_amps(self.handle, int(start), int(amps.size), ptr(amps)))
 
+    def set_histogram(self, bins: int, lo: float = 0.0, hi: float = 1.0) -> None:
+        """p-weighted E histogram of the next reducing pass (bins = 0: off)."""
+        check(lib().lrq_set_histogram(self.handle, int(bins), float(lo), float(hi)))
+        self.hist_bins = int(bins)
+
+    def histogram(self) -> np.ndarray:
+        """Raw fixed-point bins (units of 2^-60 probability; collective on ranks)."""
+        out = np.zeros(max(1, getattr(self, "hist_bins", 0)), dtype=np.uint64)
+        check(lib().lrq_get_histogram(self.handle, ptr(out)))
+        return out
+
     def set_timing(self, on: bool) -> None:
         check(lib().lrq_set_timing(self.handle, 1 if on else 0))
 
@@ -384,6 +442,38 @@ def cut_values(n: int, w: np.ndarray, z: np.ndarray | None = None, start: int = 
     out = np.empty(count, dtype=np.float64)
     if count:
         check(lib().lrq_cut_values(n, ptr(w), ptr(z) if z is not None else None, start, count, ptr(out), dev))
+    return out
+
+
+def cut_values_spin(n: int, w: np.ndarray, half_total: float, start: int, count: int,
+                    device: int | None = None) -> np.ndarray:
+    """Spin-form cut values of [start, start+count) (lrq_cut_values_spin)."""
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    dev = default_device() if device is None else device
+    out = np.empty(int(count), dtype=np.float64)
+    if count:
+        check(lib().lrq_cut_values_spin(n, ptr(w), float(half_total), int(start), int(count), ptr(out), dev))
+    return out
+
+
+def expected_cut_chunks(n: int, w: np.ndarray, half_total: float, probs: np.ndarray,
+                        device: int | None = None) -> np.ndarray:
+    """Per-2^16-chunk sums of p_z C(z) (lrq_expected_cut)."""
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    probs = np.ascontiguousarray(probs, dtype=np.float64)
+    dev = default_device() if device is None else device
+    out = np.empty(max(1, probs.size >> 16), dtype=np.float64)
+    check(lib().lrq_expected_cut(n, ptr(w), float(half_total), ptr(probs), probs.size, ptr(out), dev))
+    return out
+
+
+def draw_indices(probs: np.ndarray, u: np.ndarray, device: int | None = None) -> np.ndarray:
+    """Inverse-CDF draws over an explicit float64 distribution (lrq_draw_indices)."""
+    probs = np.ascontiguousarray(probs, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    dev = default_device() if device is None else device
+    out = np.empty(u.size, dtype=np.uint64)
+    check(lib().lrq_draw_indices(ptr(probs), probs.size, ptr(u), u.size, ptr(out), dev))
     return out
 
 

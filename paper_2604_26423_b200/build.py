@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "liblrq.so")
 SOURCES = ["lrq_engine.cu"]
-HEADERS = ["lrq_device.cuh", "lrq_sweep.cuh", "lrq_sweep_kernel.cuh", "lrq_sweep_tma.cuh", "lrq_aux.cuh", "lrq_plan.h", "lrq_dist.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-DLRQ_EXPLICIT_FFMA2", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]

@@ -33,6 +33,10 @@ struct SmallParams {
   double* red_pE;
   double* red_minE;
   unsigned long long* red_arg;
+  double* red_maxE;              // may be null
+  unsigned long long* hist;      // global energy histogram (may be null), see SweepParams
+  int hist_bins;
+  double hist_lo, hist_scale;
 };
 
 template <typename T>
@@ -41,7 +45,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = P.n, N = 1 << n;
   V* s = reinterpret_cast<V*>(smem);
-  double* red = reinterpret_cast<double*>(s + N);  // 8 warps * 4
+  double* red = reinterpret_cast<double*>(s + N);  // 8 warps * 5
   const int t = threadIdx.x;
   const int b = blockIdx.x;  // trajectory (batch); 0 for a single state
   const V* g0 = reinterpret_cast<const V*>(P.amps);
@@ -96,6 +100,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   for (int z = t; z < N; z += blockDim.x) g[z] = s[z];
   if (P.W == nullptr) return;
   double sp = 0.0, spe = 0.0, mine = __longlong_as_double(0x7ff0000000000000ll);
+  double maxe = -mine;
   unsigned long long zb = ~0ull;
   for (int z = t; z < N; z += blockDim.x) {
     double e = 0.0;
@@ -104,6 +109,8 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
     const double pv = prob(s[z]);
     sp += pv;
     spe = fma(pv, e, spe);
+    maxe = fmax(maxe, e);
+    if (P.hist) hist_add(P.hist, P.hist_bins, P.hist_lo, P.hist_scale, e, pv);
     const bool ok = P.min_bit == -1 || (P.min_bit >= 0 && !((z >> P.min_bit) & 1));
     if (ok && (e < mine || (e == mine && (unsigned long long)z < zb))) {
       mine = e;
@@ -119,31 +126,35 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
       mine = om;
       zb = oz;
     }
+    maxe = fmax(maxe, __shfl_xor_sync(0xffffffffu, maxe, o));
   }
   if ((t & 31) == 0) {
-    red[(t >> 5) * 4 + 0] = sp;
-    red[(t >> 5) * 4 + 1] = spe;
-    red[(t >> 5) * 4 + 2] = mine;
-    red[(t >> 5) * 4 + 3] = __longlong_as_double((long long)zb);
+    red[(t >> 5) * 5 + 0] = sp;
+    red[(t >> 5) * 5 + 1] = spe;
+    red[(t >> 5) * 5 + 2] = mine;
+    red[(t >> 5) * 5 + 3] = __longlong_as_double((long long)zb);
+    red[(t >> 5) * 5 + 4] = maxe;
   }
   __syncthreads();
   if (t == 0) {
-    double s0 = 0.0, s1 = 0.0, mn = red[2];
+    double s0 = 0.0, s1 = 0.0, mn = red[2], mx = red[4];
     unsigned long long b = (unsigned long long)__double_as_longlong(red[3]);
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      s0 += red[w * 4];
-      s1 += red[w * 4 + 1];
-      const double om = red[w * 4 + 2];
-      const unsigned long long oz = (unsigned long long)__double_as_longlong(red[w * 4 + 3]);
+      s0 += red[w * 5];
+      s1 += red[w * 5 + 1];
+      const double om = red[w * 5 + 2];
+      const unsigned long long oz = (unsigned long long)__double_as_longlong(red[w * 5 + 3]);
       if (om < mn || (om == mn && oz < b)) {
         mn = om;
         b = oz;
       }
+      mx = fmax(mx, red[w * 5 + 4]);
     }
     P.red_p[0] = s0;
     P.red_pE[0] = s1;
     P.red_minE[0] = mn;
     P.red_arg[0] = b;
+    if (P.red_maxE) P.red_maxE[0] = mx;
   }
 }
 
@@ -155,13 +166,14 @@ __global__ void __launch_bounds__(1024) finalize_kernel(long long T, const doubl
                                                          const double* __restrict__ rpe,
                                                          const double* __restrict__ rmin,
                                                          const unsigned long long* __restrict__ rarg,
+                                                         const double* __restrict__ rmax,
                                                          double* __restrict__ prefix, double* __restrict__ out) {
-  __shared__ double s_p[1024], s_pe[1024], s_min[1024];
+  __shared__ double s_p[1024], s_pe[1024], s_min[1024], s_max[1024];
   __shared__ unsigned long long s_arg[1024];
   const int t = threadIdx.x, NTH = blockDim.x;
   const long long per = (T + NTH - 1) / NTH;
   const long long lo = min(T, per * t), hi = min(T, lo + per);
-  double a = 0.0, b = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  double a = 0.0, b = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
   unsigned long long z = ~0ull;
   for (long long i = lo; i < hi; ++i) {
     a += rp[i];
@@ -171,14 +183,16 @@ __global__ void __launch_bounds__(1024) finalize_kernel(long long T, const doubl
       mn = m;
       z = rarg[i];
     }
+    mx = fmax(mx, rmax[i]);
   }
   s_p[t] = a;
   s_pe[t] = b;
   s_min[t] = mn;
   s_arg[t] = z;
+  s_max[t] = mx;
   __syncthreads();
   if (t == 0) {
-    double acc = 0.0, accb = 0.0, m = s_min[0];
+    double acc = 0.0, accb = 0.0, m = s_min[0], M = s_max[0];
     unsigned long long zz = s_arg[0];
     for (int i = 0; i < NTH; ++i) {
       const double x = s_p[i];
@@ -189,11 +203,13 @@ __global__ void __launch_bounds__(1024) finalize_kernel(long long T, const doubl
         m = s_min[i];
         zz = s_arg[i];
       }
+      M = fmax(M, s_max[i]);
     }
     out[0] = acc;
     out[1] = accb;
     out[2] = m;
     out[3] = __longlong_as_double((long long)zz);
+    out[4] = M;
     prefix[T] = acc;
   }
   __syncthreads();
@@ -213,14 +229,15 @@ __global__ void __launch_bounds__(256) finalize_blocks(long long T, long long pe
                                                        const double* __restrict__ rpe,
                                                        const double* __restrict__ rmin,
                                                        const unsigned long long* __restrict__ rarg,
+                                                       const double* __restrict__ rmax,
                                                        double* __restrict__ prefix, double* __restrict__ bs) {
-  __shared__ double s_p[256], s_pe[256], s_min[256];
+  __shared__ double s_p[256], s_pe[256], s_min[256], s_max[256];
   __shared__ unsigned long long s_arg[256];
   const int b = blockIdx.x, t = threadIdx.x;
   const long long lo = min(T, (long long)b * per_block), hi = min(T, lo + per_block);
   const long long per_t = (hi - lo + 255) / 256;
   const long long tlo = min(hi, lo + per_t * t), thi = min(hi, tlo + per_t);
-  double a = 0.0, c = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  double a = 0.0, c = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
   unsigned long long z = ~0ull;
   for (long long i = tlo; i < thi; ++i) {
     a += rp[i];
@@ -229,14 +246,16 @@ __global__ void __launch_bounds__(256) finalize_blocks(long long T, long long pe
       mn = rmin[i];
       z = rarg[i];
     }
+    mx = fmax(mx, rmax[i]);
   }
   s_p[t] = a;
   s_pe[t] = c;
   s_min[t] = mn;
   s_arg[t] = z;
+  s_max[t] = mx;
   __syncthreads();
   if (t == 0) {
-    double acc = 0.0, accb = 0.0, m = s_min[0];
+    double acc = 0.0, accb = 0.0, m = s_min[0], M = s_max[0];
     unsigned long long zz = s_arg[0];
     for (int i = 0; i < 256; ++i) {
       const double x = s_p[i];
@@ -247,11 +266,13 @@ __global__ void __launch_bounds__(256) finalize_blocks(long long T, long long pe
         m = s_min[i];
         zz = s_arg[i];
       }
+      M = fmax(M, s_max[i]);
     }
     bs[b] = acc;
     bs[kFinBlocks + b] = accb;
     bs[2 * kFinBlocks + b] = m;
     bs[3 * kFinBlocks + b] = __longlong_as_double((long long)zz);
+    bs[5 * kFinBlocks + b] = M;
   }
   __syncthreads();
   double run = s_p[t];
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(256) finalize_blocks(long long T, long long pe
 __global__ void finalize_combine(int nb, long long T, double* __restrict__ bs, double* __restrict__ prefix,
                                  double* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double acc = 0.0, accb = 0.0, m = bs[2 * kFinBlocks];
+  double acc = 0.0, accb = 0.0, m = bs[2 * kFinBlocks], M = bs[5 * kFinBlocks];
   unsigned long long zz = (unsigned long long)__double_as_longlong(bs[3 * kFinBlocks]);
   for (int i = 0; i < nb; ++i) {
     const double x = bs[i];
@@ -277,11 +298,13 @@ __global__ void finalize_combine(int nb, long long T, double* __restrict__ bs, d
       m = mi;
       zz = zi;
     }
+    M = fmax(M, bs[5 * kFinBlocks + i]);
   }
   out[0] = acc;
   out[1] = accb;
   out[2] = m;
   out[3] = __longlong_as_double((long long)zz);
+  out[4] = M;
   prefix[T] = acc;
 }
 
@@ -417,22 +440,29 @@ __global__ void __launch_bounds__(256) batch_sample_kernel(const double* __restr
 // Two-level inverse-CDF sampler (reference engine.py:254-263: first index
 // whose normalised cumulative probability exceeds u).  One warp per shot:
 // binary search over tile prefixes, then an in-tile scan in index order.
-template <typename T>
+// Src gives the probability of element e (|a_e|^2 of a state, or an explicit
+// float64 distribution for draw_indices); `count` bounds a short last tile.
 // Multi-GPU: this shard's CDF starts at goff of a global mass gtotal; it owns
 // the uniforms in [goff, goff + its mass) / gtotal and writes 0 for the rest
 // (the ranks' outputs are then summed); indices get the rank bits base_index.
-__global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tiles, const double* __restrict__ prefix,
-                              const double* __restrict__ u, long long shots, double goff, double gtotal,
-                              unsigned long long base_index, unsigned long long* __restrict__ out) {
-  typedef typename CxT<T>::V V;
-  const V* amps = reinterpret_cast<const V*>(amps_);
+template <typename T>
+struct AmpProb {
+  const typename CxT<T>::V* a;
+  __device__ __forceinline__ double operator()(long long e) const { return prob(a[e]); }
+};
+struct RawProb {
+  const double* p;
+  __device__ __forceinline__ double operator()(long long e) const { return p[e]; }
+};
+
+template <typename Src>
+__device__ __forceinline__ void sample_one(const Src& src, int tile_bits, long long T_tiles, long long count,
+                                           const double* __restrict__ prefix, double x, double goff, double gtotal,
+                                           unsigned long long base_index, unsigned long long* out) {
   const int lane = threadIdx.x & 31;
-  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (warp >= shots) return;
   const double total = gtotal;
-  const double x = u[warp];
   if (!(goff / total <= x && (goff + prefix[T_tiles]) / total > x)) {
-    if (lane == 0) out[warp] = 0ull;
+    if (lane == 0) *out = 0ull;
     return;
   }
   // first tile b with (goff + prefix[b+1]) / total > x
@@ -443,13 +473,13 @@ __global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tile
     else lo = mid + 1;
   }
   const long long b = lo;
-  const long long L = 1ll << tile_bits;
-  const long long chunk = L >= 32 ? L / 32 : 1;
+  const long long t0 = b << tile_bits;
+  const long long L = (count - t0) < (1ll << tile_bits) ? (count - t0) : (1ll << tile_bits);
+  const long long chunk = (L + 31) / 32;
   const long long e0 = lane * chunk;
+  const long long e1 = e0 + chunk < L ? e0 + chunk : L;
   double mine = 0.0;
-  const V* base = amps + (b << tile_bits);
-  if (e0 < L)
-    for (long long e = e0; e < e0 + chunk; ++e) mine += prob(base[e]);
+  for (long long e = e0; e < e1; ++e) mine += src(t0 + e);
   // inclusive scan over lanes
   double inc = mine;
   for (int o = 1; o < 32; o <<= 1) {
@@ -459,25 +489,61 @@ __global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tile
   const double off = goff + prefix[b];
   const bool hit = e0 < L && (off + inc) / total > x;
   const unsigned ballot = __ballot_sync(0xffffffffu, hit);
-  long long idx;
   if (ballot == 0) {
-    idx = (b << tile_bits) + L - 1;
-    if (lane == 0) out[warp] = base_index + (unsigned long long)idx;
+    if (lane == 0) *out = base_index + (unsigned long long)(t0 + L - 1);
     return;
   }
   const int L0 = __ffs(ballot) - 1;
   if (lane == L0) {
     double c = off + inc - mine;
-    idx = e0 + chunk - 1;
-    for (long long e = e0; e < e0 + chunk; ++e) {
-      c += prob(base[e]);
+    long long idx = e1 - 1;
+    for (long long e = e0; e < e1; ++e) {
+      c += src(t0 + e);
       if (c / total > x) {
         idx = e;
         break;
       }
     }
-    out[warp] = base_index + (unsigned long long)((b << tile_bits) + idx);
+    *out = base_index + (unsigned long long)(t0 + idx);
   }
+}
+
+template <typename T>
+__global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tiles, const double* __restrict__ prefix,
+                              const double* __restrict__ u, long long shots, double goff, double gtotal,
+                              unsigned long long base_index, unsigned long long* __restrict__ out) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= shots) return;
+  AmpProb<T> src{reinterpret_cast<const typename CxT<T>::V*>(amps_)};
+  sample_one(src, tile_bits, T_tiles, T_tiles << tile_bits, prefix, u[warp], goff, gtotal, base_index, out + warp);
+}
+
+// draw_indices over an explicit distribution (engine.py:254-263)
+__global__ void sample_probs_kernel(const double* __restrict__ p, long long count, int tile_bits, long long T_tiles,
+                                    const double* __restrict__ prefix, const double* __restrict__ u, long long shots,
+                                    unsigned long long* __restrict__ out) {
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= shots) return;
+  RawProb src{p};
+  sample_one(src, tile_bits, T_tiles, count, prefix, u[warp], 0.0, prefix[T_tiles], 0ull, out + warp);
+}
+
+// per-tile sums of an explicit distribution (one warp per tile, lane chunks
+// in index order, then the lane partials in lane order: deterministic)
+__global__ void prob_tile_sums_kernel(const double* __restrict__ p, long long count, int tile_bits, long long T_tiles,
+                                      double* __restrict__ tsum) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= T_tiles) return;
+  const long long t0 = warp << tile_bits;
+  const long long L = (count - t0) < (1ll << tile_bits) ? (count - t0) : (1ll << tile_bits);
+  const long long chunk = (L + 31) / 32;
+  const long long e0 = lane * chunk, e1 = e0 + chunk < L ? e0 + chunk : L;
+  double s = 0.0;
+  for (long long e = e0; e < e1; ++e) s += p[t0 + e];
+  double tot = 0.0;
+  for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, s, l);
+  if (lane == 0) tsum[warp] = tot;
 }
 
 // ---------------------------------------------------------------------------
@@ -504,6 +570,61 @@ __global__ void cut_values_kernel(int n, const double* __restrict__ w, const uns
     }
     out[k] = acc;
   }
+}
+
+
+// Spin-form cut values (reference cut_values_range, problem.py:158-171):
+// C(z) = W/2 - (1/4) s^T A s with s_k = 1 - 2 bit_k(z), A the symmetric weight
+// matrix.  t_i = sum_j s_j A_ji (j ascending), quad = sum_i t_i s_i (i
+// ascending), each add rounded in order.  The reference's own order is the
+// BLAS product's, so the two agree to ~1e-15 relative, not bitwise (the
+// bit-exact values are cut_values_kernel's).
+__device__ __forceinline__ double cut_spin(int n, const double* __restrict__ A, double half_total,
+                                           unsigned long long z) {
+  double quad = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double* Ai = A + i * n;
+    double t = 0.0;
+    for (int j = 0; j < n; ++j) t = __dadd_rn(t, ((z >> j) & 1ull) ? -Ai[j] : Ai[j]);
+    quad = __dadd_rn(quad, ((z >> i) & 1ull) ? -t : t);
+  }
+  return __dadd_rn(half_total, -0.25 * quad);
+}
+
+__global__ void cut_values_spin_kernel(int n, const double* __restrict__ A, double half_total,
+                                       unsigned long long start, long long count, double* __restrict__ out) {
+  extern __shared__ double As[];
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[i] = A[i];
+  __syncthreads();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count;
+       k += (long long)gridDim.x * blockDim.x)
+    out[k] = cut_spin(n, As, half_total, start + (unsigned long long)k);
+}
+
+// expected_r_from_probs numerator (engine.py:214-226): for each 2^16 chunk c,
+// sums[c] = sum_{z in chunk} p_z C_spin(z), combined in a fixed tree order
+// (one CTA per chunk); the host adds the chunk sums in chunk order.
+__global__ void __launch_bounds__(256) expected_cut_kernel(int n, const double* __restrict__ A, double half_total,
+                                                           const double* __restrict__ p, long long count,
+                                                           int chunk_bits, double* __restrict__ sums) {
+  extern __shared__ double As[];
+  __shared__ double part[256];
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[i] = A[i];
+  __syncthreads();
+  const long long c0 = (long long)blockIdx.x << chunk_bits;
+  const long long c1 = c0 + (1ll << chunk_bits) < count ? c0 + (1ll << chunk_bits) : count;
+  double acc = 0.0;
+  for (long long z = c0 + threadIdx.x; z < c1; z += blockDim.x) {
+    const double pz = p[z];
+    if (pz != 0.0) acc = fma(pz, cut_spin(n, As, half_total, (unsigned long long)z), acc);
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[blockIdx.x] = part[0];
 }
 
 }  // namespace lrq

@@ -149,11 +149,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
       : "memory");
   return ok != 0;
 }
-// bounded wait: a lost transaction traps (a recoverable launch error) instead
-// of hanging the device (each try_wait sleeps up to 1 ms: ~10^4 s in total)
+// bounded wait: a lost transaction traps (a recoverable launch error) after
+// kMbarTrapNs of wall time instead of hanging the device.  The clock is read
+// only once the fast path has failed, so a ready barrier costs one try_wait.
+constexpr unsigned long long kMbarTrapNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  for (unsigned i = 0; !mbar_try_wait(b, parity); ++i)
-    if (i > (1u << 24)) __trap();
+  if (mbar_try_wait(b, parity)) return;
+  const unsigned long long t0 = global_ns();
+  while (!mbar_try_wait(b, parity))
+    if (global_ns() - t0 > kMbarTrapNs) __trap();
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2) {
@@ -223,5 +232,16 @@ __device__ __forceinline__ double prob(float2 a) {
   return __fma_rn(x, x, __dmul_rn(y, y));
 }
 __device__ __forceinline__ double prob(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+// p-weighted energy histogram bin update (SweepParams::hist): fixed point
+// with 2^60 per unit probability, integer atomics (order-independent sums)
+constexpr double kHistOne = 1152921504606846976.0;  // 2^60: fixed-point unit of a histogram bin
+__device__ __forceinline__ void hist_add(unsigned long long* h, int bins, double lo, double scale, double e,
+                                         double p) {
+  int b = (int)floor((e - lo) * scale);
+  b = b < 0 ? 0 : (b >= bins ? bins - 1 : b);
+  const unsigned long long q = (unsigned long long)__double2ll_rn(p * kHistOne);
+  if (q) atomicAdd(h + b, q);
+}
 
 }  // namespace lrq

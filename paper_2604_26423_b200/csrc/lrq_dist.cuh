@@ -34,6 +34,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 inline NcclApi& nccl() {
@@ -65,6 +66,7 @@ inline NcclApi& nccl() {
     LRQ_NCCL_SYM(AllGather, ncclAllGather)
     LRQ_NCCL_SYM(AllReduce, ncclAllReduce)
     LRQ_NCCL_SYM(GetErrorString, ncclGetErrorString)
+    LRQ_NCCL_SYM(CommGetAsyncError, ncclCommGetAsyncError)
 #undef LRQ_NCCL_SYM
     api.ok = true;
   });

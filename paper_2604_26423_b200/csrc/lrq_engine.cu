@@ -7,7 +7,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <chrono>
+#include <thread>
 #include <condition_variable>
 #include <mutex>
 #include <string>
@@ -39,6 +41,12 @@ int fail(int code, const std::string& msg) {
                   std::string("CUDA error in ") + #expr + ": " + cudaGetErrorString(e_));    \
     }                                                                                         \
   } while (0)
+
+// per-tile reduction arrays (sum p, sum pE, min E, argmin, max E), finalize
+// outputs (the same five scalars) and the multi-CTA finalize scratch
+constexpr int kRedArrays = 5;
+constexpr int kOutScalars = 5;
+constexpr int kFinScratch = 6 * kFinBlocks;
 
 // tile geometry: 4096 16-byte units per tile = 2^(12+pair)
 // amplitudes (pair = 1 for complex64: a unit holds two amplitudes)
@@ -133,6 +141,9 @@ struct lrq_group {
   std::vector<lrq_state*> members;
   std::vector<double> gather;               // 4 * world finalize scalars
   std::vector<const uint64_t*> shot_bufs;  // per-rank host sample buffers
+  // fused remap decision, taken once every member exists (group_prepare):
+  // second state buffers for all members, or none
+  bool decided = false, fused_ok = false;
 };
 
 struct lrq_state {
@@ -146,7 +157,7 @@ struct lrq_state {
   long long num_tiles = 1;
   double* red = nullptr;     // 4 arrays of num_tiles (p, pE, minE, arg bits)
   double* prefix = nullptr;  // num_tiles + 1
-  double* out = nullptr;     // 4 finalize scalars
+  double* out = nullptr;     // kOutScalars finalize scalars
   double* fin = nullptr;     // 5 * kFinBlocks finalize scratch
   double* dW = nullptr;      // n*n cost matrix
   double* dzero = nullptr;   // n zeros (no global qubits on a single device)
@@ -168,14 +179,19 @@ struct lrq_state {
   lrq_group* group = nullptr;      // in-process transport (lrq_create_shard)
   // fused remap: two state buffers per rank (amps == bufs[cur]); the sweep
   // before a remap writes the next buffer of every rank through peer pointers
-  void* bufs[2] = {nullptr, nullptr};
+  void* bufs[2] = {nullptr, nullptr};  // bufs[0] = the primary buffer (always), bufs[1] = fused-remap spare
   int cur = 0;
-  void* peer[2][8] = {};
-  bool fused = false;
+  void* peer[2][8] = {};  // peers' buffers (NCCL ranks: IPC-mapped; world <= 8)
+  bool fused = false;     // fused remap: both buffers of every rank mapped and tested
+  bool peer_ok = false;   // pipelined remap over peer memory: primary buffers mapped and tested
   std::vector<void*> ipc_open;  // peer buffers mapped with cudaIpcOpenMemHandle
-  float* dflag = nullptr;       // 1 float for the NCCL stream barrier
-  unsigned char* stage = nullptr;  // remap staging, (world-1) * chunk bytes
+  float* dflag = nullptr;       // 2 floats: NCCL stream barrier / pair token (send, recv)
+  float* probe = nullptr;       // IPC self-test target (world floats)
+  unsigned char* stage = nullptr;  // NCCL remap staging, chunk bytes
   size_t chunk = 0;
+  cudaStream_t cstream = nullptr;  // remap stream (pipelined exchange, overlapped with the sweep)
+  std::vector<cudaEvent_t> pev;    // world + 1 events: block j of the remap sweep done / remap done
+  bool broken = false;             // a collective failed: the communicator was aborted
   std::vector<double> cost_edges;  // global cost edges (lexicographic)
   double* dWx = nullptr;           // cost field from the rank's qubits (n_loc)
   double wcst = 0.0;
@@ -190,6 +206,11 @@ struct lrq_state {
   int fcap = 0;
   std::vector<double> rank_sum_p;  // per-rank probability mass of the last run
   double remap_ms = 0.0;
+  // p-weighted energy histogram of the reducing passes (lrq_set_histogram)
+  unsigned long long* dhist = nullptr;
+  int hist_bins = 0;
+  double hist_lo = 0.0, hist_hi = 0.0;
+  bool hist_summed = false;  // NCCL ranks: dhist already holds the sum over ranks
 };
 
 namespace {
@@ -198,13 +219,16 @@ void free_state(lrq_state* s) {
   if (!s) return;
   DeviceGuard g(s->device);
   for (void* p : s->ipc_open) cudaIpcCloseMemHandle(p);
-  if (s->bufs[1]) {
+  if (s->bufs[0]) {
     cudaFree(s->bufs[0]);
     cudaFree(s->bufs[1]);
   } else {
     cudaFree(s->amps);
   }
   cudaFree(s->dflag);
+  cudaFree(s->probe);
+  for (cudaEvent_t e : s->pev) cudaEventDestroy(e);
+  if (s->cstream) cudaStreamDestroy(s->cstream);
   cudaFree(s->red);
   cudaFree(s->prefix);
   cudaFree(s->out);
@@ -220,6 +244,7 @@ void free_state(lrq_state* s) {
   cudaFree(s->dF);
   cudaFree(s->dmsign);
   cudaFree(s->dgather);
+  cudaFree(s->dhist);
   if (s->comm && nccl().ok) nccl().CommDestroy(s->comm);
   if (s->group) {
     std::lock_guard<std::mutex> lk(s->group->mu);
@@ -454,7 +479,7 @@ int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
   SweepParams sp = sp_in;
   const int K = tile_amp_bits(s->pbytes);
   const int ma = group_ma(gk, pair_of(s->pbytes));
-  if (!make_tile_tmap(&sp.tmap, s->amps, gk, sp.n, s->pbytes, ma, K, sp.q0, s->num_tiles))
+  if (!make_tile_tmap(&sp.tmap, sp.amps, gk, sp.n, s->pbytes, ma, K, sp.q0, sp.num_tiles))
     return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
   sp.has_tmap = 1;
   sp.nstages = 3;
@@ -464,7 +489,7 @@ int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
   const size_t smem = wd_smem_bytes(sp.n, 3, sk == SK_F || sk == SK_P);
   if (smem > 227 * 1024) return fail(LRQ_ERUNTIME, "internal: warp-decoupled sweep needs too much shared memory");
   const int sms = sm_count(s->device);
-  const int g = (int)(s->num_tiles < sms ? s->num_tiles : sms);
+  const int g = (int)(sp.num_tiles < sms ? sp.num_tiles : sms);
   if (s->pbytes == 16) {
     if (gk != GK_H) return fail(LRQ_ERUNTIME, "internal: complex128 warp-decoupled sweeps need an H group");
     return launch_wd_kind<double, GK_H>(s->stream, sk, sp, g, smem);
@@ -477,12 +502,12 @@ int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int gri
   const bool amps = sk != SK_N;
   const bool usesJ = sk == SK_P || sk == SK_F || sk == SK_L;
   const bool usesW = sk == SK_R || sk == SK_Q || sk == SK_N || (sk == SK_L && sp_in.reduce);
-  if (use_tma_path(s->pbytes, gk, sk)) {
+  if (!sp_in.hist && use_tma_path(s->pbytes, gk, sk)) {
     // TMA-fed pipeline: one CTA per SM, a ring of 64 KB stages, 1 or 2 teams
     SweepParams sp = sp_in;
     const int K = tile_amp_bits(s->pbytes);
     const int ma = group_ma(gk, pair_of(s->pbytes));
-    if (!make_tile_tmap(&sp.tmap, s->amps, gk, sp.n, s->pbytes, ma, K, sp.q0, s->num_tiles))
+    if (!make_tile_tmap(&sp.tmap, sp.amps, gk, sp.n, s->pbytes, ma, K, sp.q0, sp.num_tiles))
       return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the sweep tile map");
     sp.has_tmap = 1;
     const size_t cap = 227 * 1024;
@@ -494,33 +519,34 @@ int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int gri
     sp.nstages = tma_smem_bytes(sp.n, 3, teams, usesJ, usesW) <= cap ? 3 : 2;
     const size_t smem = tma_smem_bytes(sp.n, sp.nstages, teams, usesJ, usesW);
     const int sms = sm_count(s->device);
-    const int g = (int)(s->num_tiles < sms ? s->num_tiles : sms);
+    const int g = (int)(sp.num_tiles < sms ? sp.num_tiles : sms);
     if (s->pbytes == 8)
       return teams == 2 ? launch_tma_any<float, 2>(s->stream, gk, sk, sp, g, smem)
                         : launch_tma_any<float, 1>(s->stream, gk, sk, sp, g, smem);
     return teams == 2 ? launch_tma_any<double, 2>(s->stream, gk, sk, sp, g, smem)
                       : launch_tma_any<double, 1>(s->stream, gk, sk, sp, g, smem);
   }
-  const size_t smem = sweep_smem_bytes(sp_in.n, amps, usesJ, usesW);
+  const size_t smem = sweep_smem_bytes(sp_in.n, amps, usesJ, usesW, sp_in.hist ? sp_in.hist_bins : 0);
   if (s->pbytes == 8) return launch_sweep_kind<float>(s->stream, gk, sk, sp_in, grid, smem);
   return launch_sweep_kind<double>(s->stream, gk, sk, sp_in, grid, smem);
 }
 
 // deterministic combine of the per-tile partials + CDF prefix (lrq_aux.cuh);
-// bs: 5 * kFinBlocks doubles of scratch (multi-CTA path for large T)
+// bs: kFinScratch doubles of scratch (multi-CTA path for large T)
 int launch_finalize(cudaStream_t st, long long T, double* red, double* prefix, double* out, double* bs) {
   double* rp = red;
   double* rpe = red + T;
   double* rmin = red + 2 * T;
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(red + 3 * T);
+  const double* rmax = red + 4 * T;
   if (T < 8192 || !bs) {
-    finalize_kernel<<<1, 1024, 0, st>>>(T, rp, rpe, rmin, rarg, prefix, out);
+    finalize_kernel<<<1, 1024, 0, st>>>(T, rp, rpe, rmin, rarg, rmax, prefix, out);
     CUDA_TRY(cudaGetLastError());
     return LRQ_OK;
   }
   const long long per = (T + kFinBlocks - 1) / kFinBlocks;
   const int nb = (int)((T + per - 1) / per);
-  finalize_blocks<<<nb, 256, 0, st>>>(T, per, rp, rpe, rmin, rarg, prefix, bs);
+  finalize_blocks<<<nb, 256, 0, st>>>(T, per, rp, rpe, rmin, rarg, rmax, prefix, bs);
   CUDA_TRY(cudaGetLastError());
   finalize_combine<<<1, 32, 0, st>>>(nb, T, bs, prefix, out);
   CUDA_TRY(cudaGetLastError());
@@ -558,6 +584,22 @@ void record(lrq_state* s, size_t idx, char kind) {
   if (kind) s->kinds.push_back(kind);
 }
 
+// the energy histogram of a reducing pass (lrq_set_histogram): zeroed on
+// the engine stream before the pass, filled by the pass's integer atomics
+template <typename PR>
+void set_hist(lrq_state* s, PR& sp) {
+  if (!s->dhist) return;
+  sp.hist = s->dhist;
+  sp.hist_bins = s->hist_bins;
+  sp.hist_lo = s->hist_lo;
+  sp.hist_scale = s->hist_bins / (s->hist_hi - s->hist_lo);
+}
+int zero_hist(lrq_state* s) {
+  s->hist_summed = false;
+  if (s->dhist) CUDA_TRY(cudaMemsetAsync(s->dhist, 0, sizeof(unsigned long long) * s->hist_bins, s->stream));
+  return LRQ_OK;
+}
+
 #define NCCL_TRY(expr)                                                                           \
   do {                                                                                           \
     ncclResult_t r_ = (expr);                                                                    \
@@ -565,15 +607,11 @@ void record(lrq_state* s, size_t idx, char kind) {
       return fail(LRQ_ERUNTIME, std::string("NCCL error in ") + #expr + ": " + nccl().GetErrorString(r_)); \
   } while (0)
 
-// Exchange, chunk by chunk, local block `b` (top g local bits = b) with
-// rank `b`'s block `rank`: the all-to-all block transpose that swaps the g
-// global qubits with the top g local qubits.  peer >= 0: instead swap the
-// whole local state with that one rank (used by the deferred global flip).
 // Host barrier of an in-process group (600 s limit, like the reference's
 // receive timeout, sharded.py:38).
 int group_barrier(lrq_group* G) {
   std::unique_lock<std::mutex> lk(G->mu);
-  if (G->broken) return fail(LRQ_ERUNTIME, "shard group aborted: " + G->why);
+  if (G->broken) return fail(LRQ_ERUNTIME, "aborted run: shard group: " + G->why);
   const unsigned long long my = G->gen;
   if (++G->count == G->world) {
     G->count = 0;
@@ -586,7 +624,7 @@ int group_barrier(lrq_group* G) {
     G->why = "barrier timeout";
     G->cv.notify_all();
   }
-  if (G->gen == my) return fail(LRQ_ERUNTIME, "shard group aborted: " + G->why);
+  if (G->gen == my) return fail(LRQ_ERUNTIME, "aborted run: shard group: " + G->why);
   return LRQ_OK;
 }
 
@@ -597,10 +635,24 @@ void group_abort(lrq_group* G, const std::string& why) {
   G->cv.notify_all();
 }
 
-// a[i] <-> b[i] over `bytes` (16-byte units; the blocks are 16-byte multiples)
-__global__ void swap_kernel(uint4* __restrict__ a, uint4* __restrict__ b, long long units) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < units;
-       i += (long long)gridDim.x * blockDim.x) {
+// a[i] <-> b[i] over `units` 16-byte units; four independent pairs per
+// thread and iteration keep enough NVLink reads in flight for a peer buffer
+__global__ void __launch_bounds__(256) swap_kernel(uint4* __restrict__ a, uint4* __restrict__ b, long long units) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < units; i += 4 * stride) {
+    const uint4 x0 = a[i], x1 = a[i + stride], x2 = a[i + 2 * stride], x3 = a[i + 3 * stride];
+    const uint4 y0 = b[i], y1 = b[i + stride], y2 = b[i + 2 * stride], y3 = b[i + 3 * stride];
+    a[i] = y0;
+    a[i + stride] = y1;
+    a[i + 2 * stride] = y2;
+    a[i + 3 * stride] = y3;
+    b[i] = x0;
+    b[i + stride] = x1;
+    b[i + 2 * stride] = x2;
+    b[i + 3 * stride] = x3;
+  }
+  for (; i < units; i += stride) {
     const uint4 x = a[i], y = b[i];
     a[i] = y;
     b[i] = x;
@@ -621,29 +673,181 @@ int enable_peer(int dev, int peer) {
   return LRQ_OK;
 }
 
-// exchange_blocks for an in-process group: every rank's work so far is
-// complete (stream sync + barrier); the lower rank of each pair swaps the two
-// blocks in place; a second barrier publishes the result.
-int exchange_group(lrq_state* s, int peer) {
-  lrq_group* G = s->group;
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  int rc = group_barrier(G);
-  if (rc) return rc;
-  const size_t block = peer >= 0 ? (size_t)s->pbytes << s->n : (size_t)s->pbytes << (s->n - s->g);
-  const int grid = 4 * sm_count(s->device);
-  for (int b = s->rank + 1; b < s->world; ++b) {
-    if (peer >= 0 && b != peer) continue;
-    lrq_state* o = G->members[b];
-    rc = enable_peer(s->device, o->device);
-    if (rc) return rc;
-    unsigned char* mine = reinterpret_cast<unsigned char*>(s->amps) + (peer >= 0 ? 0 : (size_t)b * block);
-    unsigned char* theirs = reinterpret_cast<unsigned char*>(o->amps) + (peer >= 0 ? 0 : (size_t)s->rank * block);
-    swap_kernel<<<grid, 256, 0, s->stream>>>(reinterpret_cast<uint4*>(mine), reinterpret_cast<uint4*>(theirs),
-                                             (long long)(block / 16));
-    CUDA_TRY(cudaGetLastError());
+// ---------------------------------------------------------------------------
+// Failure handling of NCCL ranks (reference: a failed shard worker aborts the
+// whole run with AbortedRunError, sharded.py:328-349).  Every wait on a
+// stream that carries collectives polls the communicator's async error and a
+// wall-clock limit ($LRQ_DIST_TIMEOUT_S, default 600 s like the reference's
+// receive timeout, sharded.py:38); on either the communicator is aborted
+// (ncclCommAbort, which also unblocks the NCCL kernels of this rank) and the
+// state refuses further collectives.
+int abort_comm(lrq_state* s, const std::string& why) {
+  if (s->comm && nccl().ok) nccl().CommAbort(s->comm);
+  s->comm = nullptr;
+  s->broken = true;
+  return fail(LRQ_ERUNTIME, "aborted run: " + why);
+}
+
+int dist_wait(lrq_state* s, cudaStream_t st) {
+  if (!s->comm) {
+    if (s->broken) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return LRQ_OK;
   }
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return group_barrier(G);
+  const double limit = (double)env_int("LRQ_DIST_TIMEOUT_S", 600);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned it = 0;; ++it) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return LRQ_OK;
+    if (e != cudaErrorNotReady) return abort_comm(s, std::string("CUDA error: ") + cudaGetErrorString(e));
+    ncclResult_t ae = ncclSuccess;
+    if (nccl().CommGetAsyncError(s->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+      return abort_comm(s, std::string("NCCL error on another rank or link: ") + nccl().GetErrorString(ae));
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > limit) return abort_comm(s, "no progress from the other ranks for " + std::to_string((int)limit) + " s");
+    if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+#define NCCL_TRY_S(s, expr)                                                                          \
+  do {                                                                                               \
+    ncclResult_t r_ = (expr);                                                                        \
+    if (r_ != ncclSuccess) return abort_comm((s), std::string("NCCL error in ") + #expr + ": " +    \
+                                                      nccl().GetErrorString(r_));                     \
+  } while (0)
+
+int ensure_remap_stream(lrq_state* s) {
+  if (!s->cstream) CUDA_TRY(cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking));
+  while ((int)s->pev.size() < s->world + 1) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->pev.push_back(e);
+  }
+  return LRQ_OK;
+}
+
+// One pairwise step of a remap on rank `rank`: swap my block my_block with
+// block their_block of `partner`; half = 0 / 1: the half of the pair's bytes
+// this rank moves in a peer-memory swap (lower rank: first half).
+struct RemapStep {
+  int partner;
+  int my_block, their_block;  // in blocks of the remap (-1: the whole state, the mirror exchange)
+  int half;
+};
+// XOR schedule of the all-to-all block transpose (step k = 1..world-1:
+// partner rank ^ k), or the single mirror step of the deferred global flip.
+inline std::vector<RemapStep> remap_schedule(int world, int rank, int mirror) {
+  std::vector<RemapStep> v;
+  if (mirror >= 0) {
+    v.push_back({mirror, -1, -1, rank < mirror ? 0 : 1});
+    return v;
+  }
+  for (int k = 1; k < world; ++k) {
+    const int p = rank ^ k;
+    v.push_back({p, p, rank, rank < p ? 0 : 1});
+  }
+  return v;
+}
+
+// Remap transports.  A remap swaps the g global qubits with the top g local
+// bits: local block b (top g local bits = b) of rank r trades places with
+// block r of rank b — an all-to-all block transpose done in place as G-1
+// pairwise swaps on the XOR schedule (step k: rank r <-> r ^ k; every rank has
+// exactly one partner per step, and block r^k of r pairs with block r of r^k).
+// `mirror` >= 0 instead swaps the whole local state with that one rank (the
+// deferred global flip).  Transports, chosen at setup:
+//   group  in-process shards: a swap kernel over the members' buffers (same
+//          device or peer access); host barriers order the ranks;
+//   peer   NCCL ranks whose primary buffers are IPC-mapped: a 1-float
+//          send/recv token pairs the two ranks, then each swaps its half of
+//          the two blocks in place over NVLink (no staging, no copy);
+//   nccl   otherwise: chunked ncclSend/ncclRecv into one staging chunk, then
+//          a device copy into the block.
+// Each rank calls pair_exchange with mirrored offsets; the lower rank of the
+// pair takes the first half of a peer-memory swap, the higher one the rest.
+int pair_exchange(lrq_state* s, int p, size_t my_off, size_t their_off, size_t bytes, int which_half,
+                  cudaStream_t st) {
+  unsigned char* mine = reinterpret_cast<unsigned char*>(s->amps) + my_off;
+  const int grid = 2 * sm_count(s->device);
+  if (s->group || s->peer_ok) {
+    unsigned char* theirs = nullptr;
+    if (s->group) {
+      lrq_state* o = s->group->members[p];
+      if (!o) return fail(LRQ_ERUNTIME, "aborted run: shard group member missing");
+      const int rc = enable_peer(s->device, o->device);
+      if (rc) return rc;
+      theirs = reinterpret_cast<unsigned char*>(o->amps) + their_off;
+    } else {
+      // pair token: the partner has reached this step (its blocks are final)
+      NCCL_TRY_S(s, nccl().GroupStart());
+      NCCL_TRY_S(s, nccl().Send(s->dflag, 1, ncclFloat, p, s->comm, st));
+      NCCL_TRY_S(s, nccl().Recv(s->dflag + 1, 1, ncclFloat, p, s->comm, st));
+      NCCL_TRY_S(s, nccl().GroupEnd());
+      theirs = reinterpret_cast<unsigned char*>(s->peer[0][p]) + their_off;
+    }
+    const size_t half = (bytes / 2) & ~(size_t)15;
+    const size_t off = which_half == 0 ? 0 : half, len = which_half == 0 ? half : bytes - half;
+    swap_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<uint4*>(mine + off), reinterpret_cast<uint4*>(theirs + off),
+                                      (long long)(len / 16));
+    CUDA_TRY(cudaGetLastError());
+    return LRQ_OK;
+  }
+  NcclApi& nc = nccl();
+  for (size_t o = 0; o < bytes; o += s->chunk) {
+    const size_t len = bytes - o < s->chunk ? bytes - o : s->chunk;
+    NCCL_TRY_S(s, nc.GroupStart());
+    NCCL_TRY_S(s, nc.Send(mine + o, len, ncclUint8, p, s->comm, st));
+    NCCL_TRY_S(s, nc.Recv(s->stage, len, ncclUint8, p, s->comm, st));
+    NCCL_TRY_S(s, nc.GroupEnd());
+    CUDA_TRY(cudaMemcpyAsync(mine + o, s->stage, len, cudaMemcpyDeviceToDevice, st));
+  }
+  return LRQ_OK;
+}
+
+// The whole remap (or the mirror exchange).  pipelined: the blocks come from
+// a sweep split by block on the engine stream, block r^k marked by event
+// pev[k]; the swaps run on the remap stream as the blocks complete, and the
+// engine stream waits for the last one.  Otherwise the sweep has finished on
+// the engine stream and the swaps follow on it.
+int remap_exchange(lrq_state* s, bool pipelined, int mirror) {
+  const bool grp = s->group != nullptr;
+  if (!grp && !s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
+  int rc = ensure_remap_stream(s);
+  if (rc) return rc;
+  cudaStream_t st = pipelined ? s->cstream : s->stream;
+  const size_t block = (size_t)s->pbytes << (s->n - s->g), whole = (size_t)s->pbytes << s->n;
+  if (grp && !pipelined) {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if ((rc = group_barrier(s->group))) return rc;
+  }
+  const std::vector<RemapStep> steps = remap_schedule(s->world, s->rank, mirror);
+  for (int k = 1; k <= (int)steps.size(); ++k) {
+    const RemapStep& sp = steps[k - 1];
+    const int p = sp.partner;
+    if (pipelined) {
+      if (grp) {
+        CUDA_TRY(cudaEventSynchronize(s->pev[k]));
+        if ((rc = group_barrier(s->group))) return rc;
+      } else {
+        CUDA_TRY(cudaStreamWaitEvent(st, s->pev[k], 0));
+      }
+    }
+    if (sp.my_block < 0) rc = pair_exchange(s, p, 0, 0, whole, sp.half, st);
+    else rc = pair_exchange(s, p, (size_t)sp.my_block * block, (size_t)sp.their_block * block, block, sp.half, st);
+    if (rc) return rc;
+  }
+  if (grp) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return group_barrier(s->group);  // every member's swaps into our blocks are done
+  }
+  // peer transport: the partners write into our blocks; the all-reduce on the
+  // same stream completes only after every rank's swap kernels
+  if (s->peer_ok) NCCL_TRY_S(s, nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, st));
+  if (pipelined) {
+    CUDA_TRY(cudaEventRecord(s->pev[s->world], st));
+    CUDA_TRY(cudaStreamWaitEvent(s->stream, s->pev[s->world], 0));
+  }
+  return LRQ_OK;
 }
 
 // the sampler's sum over ranks for an in-process group (host buffers)
@@ -664,42 +868,78 @@ int group_sum_shots(lrq_state* s, uint64_t* idx, int64_t shots) {
   return LRQ_OK;
 }
 
-int exchange_blocks(lrq_state* s, int peer) {
-  if (s->group) return exchange_group(s, peer);
-  NcclApi& nc = nccl();
-  const size_t block = peer >= 0 ? (size_t)s->pbytes << s->n : (size_t)s->pbytes << (s->n - s->g);
-  unsigned char* base = reinterpret_cast<unsigned char*>(s->amps);
-  for (size_t off = 0; off < block; off += s->chunk) {
-    const size_t len = block - off < s->chunk ? block - off : s->chunk;
-    NCCL_TRY(nc.GroupStart());
-    int slot = 0;
-    for (int b = 0; b < s->world; ++b) {
-      if (b == s->rank || (peer >= 0 && b != peer)) continue;
-      const size_t at = (peer >= 0 ? 0 : (size_t)b * block) + off;
-      NCCL_TRY(nc.Send(base + at, len, ncclUint8, b, s->comm, s->stream));
-      NCCL_TRY(nc.Recv(s->stage + (size_t)slot * s->chunk, len, ncclUint8, b, s->comm, s->stream));
-      ++slot;
-    }
-    NCCL_TRY(nc.GroupEnd());
-    slot = 0;
-    for (int b = 0; b < s->world; ++b) {
-      if (b == s->rank || (peer >= 0 && b != peer)) continue;
-      const size_t at = (peer >= 0 ? 0 : (size_t)b * block) + off;
-      CUDA_TRY(cudaMemcpyAsync(base + at, s->stage + (size_t)slot * s->chunk, len, cudaMemcpyDeviceToDevice,
-                               s->stream));
-      ++slot;
+// Device memory a rank needs besides the state: tile reductions + CDF prefix,
+// finalize scratch, cost matrices, NCCL staging.  Host-side accounting shared
+// by create_rank_state and lrq_describe_memory.
+size_t remap_chunk(size_t block) { return block < (256ull << 20) ? block : (256ull << 20); }
+size_t rank_extra_bytes(int n_loc, int pbytes, int world, int p, bool staging) {
+  const long long T = n_loc >= tile_amp_bits(pbytes) ? (1ll << (n_loc - tile_amp_bits(pbytes))) : 1;
+  int g = 0;
+  while ((1 << g) < world) ++g;
+  size_t b = 8ull * (4 * T + T + 1) + 8ull * (4 + 5 * kFinBlocks);     // red, prefix, out, fin
+  b += 8ull * n_loc * n_loc + 8ull * (n_loc + 1) + 8ull * n_loc;        // dW, dzero, dWx
+  b += 8ull * ((size_t)n_loc * n_loc + n_loc) * 2 * (p > 0 ? p : 1);     // dJ (both permutation states)
+  b += 8ull * 4 * world + 2 * 4 + 4ull * world;                          // dgather, dflag, probe
+  if (staging) b += remap_chunk((size_t)pbytes << (n_loc - g));
+  return b;
+}
+
+// In-process groups: decide once, with every member present, whether all
+// members get the second (fused-remap) buffer: only if, on every device, the
+// members' spare buffers fit with 2 GiB to spare.  Otherwise no member gets
+// one and remaps take the pipelined swap.
+void group_prepare(lrq_state* s) {
+  lrq_group* G = s->group;
+  std::lock_guard<std::mutex> lk(G->mu);
+  if (G->decided) return;
+  for (lrq_state* m : G->members)
+    if (!m) return;  // not every shard exists yet: decide later
+  G->decided = true;
+  G->fused_ok = false;
+  if (!env_int("LRQ_FUSED_REMAP", 1) || G->world > 8) return;
+  std::vector<int> devs;
+  for (lrq_state* m : G->members)
+    if (std::find(devs.begin(), devs.end(), m->device) == devs.end()) devs.push_back(m->device);
+  for (int d : devs) {
+    size_t need = 2ull << 30;
+    for (lrq_state* m : G->members)
+      if (m->device == d) need += m->state_bytes;
+    DeviceGuard dg(d);
+    size_t freeb = 0, totalb = 0;
+    if (cudaMemGetInfo(&freeb, &totalb) != cudaSuccess || freeb < need) {
+      cudaGetLastError();
+      return;
     }
   }
-  return LRQ_OK;
+  bool ok = true;
+  for (lrq_state* m : G->members) {
+    DeviceGuard dg(m->device);
+    void* alt = nullptr;
+    if (cudaMalloc(&alt, m->state_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      break;
+    }
+    m->bufs[1] = alt;
+  }
+  if (!ok)
+    for (lrq_state* m : G->members) {
+      DeviceGuard dg(m->device);
+      cudaFree(m->bufs[1]);
+      m->bufs[1] = nullptr;
+    }
+  G->fused_ok = ok;
 }
 
 // fused remap availability: both state buffers on every rank and the peers'
 // buffers addressable (in-process groups: the members' pointers, with peer
 // access across devices; NCCL ranks: mapped by lrq_fused_setup)
 bool fused_ready(lrq_state* s) {
-  if (!s->bufs[1] || !env_int("LRQ_FUSED_REMAP", 1)) return false;
+  if (!env_int("LRQ_FUSED_REMAP", 1)) return false;
   if (s->group) {
+    group_prepare(s);
     lrq_group* G = s->group;
+    if (!G->fused_ok) return false;
     for (int b = 0; b < s->world; ++b) {
       lrq_state* o = G->members[b];
       if (!o || !o->bufs[1] || o->cur != s->cur) return false;
@@ -715,7 +955,7 @@ bool fused_ready(lrq_state* s) {
     }
     return true;
   }
-  return s->fused;
+  return s->fused && s->bufs[1];
 }
 
 // all ranks' fused-remap stores are complete before anyone reads its buffer
@@ -725,7 +965,7 @@ int fused_barrier(lrq_state* s) {
     return group_barrier(s->group);
   }
   // stream-ordered: the all-reduce completes only after every rank's sweep
-  NCCL_TRY(nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));
+  NCCL_TRY_S(s, nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));
   return LRQ_OK;
 }
 
@@ -757,6 +997,7 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
   double* rpe = rp + s->num_tiles;
   double* rmin = rpe + s->num_tiles;
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
+  double* rmax = rmin + 2 * s->num_tiles;
   // the final pass runs in the identity permutation: the top logical qubit is
   // rank bit g-1 (max-cut search over top bit 0)
   const int min_bit = ((s->rank >> (g - 1)) & 1) ? -2 : -1;
@@ -776,7 +1017,7 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
       if (s->pbytes == 8) reverse_kernel<float2><<<blocks, 256, 0, s->stream>>>(s->amps, nl);
       else reverse_kernel<double2><<<blocks, 256, 0, s->stream>>>(s->amps, nl);
       CUDA_TRY(cudaGetLastError());
-      int rc = exchange_blocks(s, s->world - 1 - s->rank);
+      int rc = remap_exchange(s, false, s->world - 1 - s->rank);
       if (rc) return rc;
       record(s, ev++, 'X');
     }
@@ -813,6 +1054,11 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
+    sp.red_maxE = rmax;
+    if (w.reduce) {
+      if (const int rh = zero_hist(s)) return rh;
+      set_hist(s, sp);
+    }
     // (a tile must lie inside one destination block: n_loc - g >= tile bits)
     const bool fuse = w.remap_after && fused && gr.kind == GK_A && w.kind == SK_M && nl - g >= P.KA;
     if (fuse) {
@@ -826,12 +1072,33 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.rbits = tb - g;
       for (int b = 0; b < s->world; ++b) sp.rdst[b] = (char*)s->peer[next][b] + (size_t)s->rank * blockBytes;
     }
-    int rc = w.prog == 1 ? launch_wd(s, gr.kind, w.kind, sp)
-             : fuse      ? (s->pbytes == 8 ? launch_sweep_kind<float>(s->stream, gr.kind, w.kind, sp, grid,
-                                                                       sweep_smem_bytes(nl, true, false, false))
-                                           : launch_sweep_kind<double>(s->stream, gr.kind, w.kind, sp, grid,
-                                                                        sweep_smem_bytes(nl, true, false, false)))
-                         : launch_sweep(s, gr.kind, w.kind, sp, grid);
+    // pipelined remap: the group-A sweep runs block by block in XOR order
+    // (block rank ^ j at step j) and each finished block is swapped with its
+    // owner while the next block is swept (remap_exchange on the remap stream)
+    const bool pipe = !fuse && w.remap_after && gr.kind == GK_A && w.kind == SK_M && nl - g >= P.KA &&
+                      env_int("LRQ_PIPELINED_REMAP", 1);
+    int rc = LRQ_OK;
+    if (pipe) {
+      if ((rc = ensure_remap_stream(s))) return rc;
+      const long long TB = s->num_tiles >> g;
+      const size_t blockBytes = (size_t)s->pbytes << (nl - g);
+      for (int j = 0; j < s->world && !rc; ++j) {
+        SweepParams sb = sp;
+        sb.amps = reinterpret_cast<char*>(s->amps) + (size_t)(s->rank ^ j) * blockBytes;
+        sb.num_tiles = TB;
+        rc = launch_sweep(s, gr.kind, w.kind, sb, (int)(TB < grid ? TB : grid));
+        if (!rc && cudaEventRecord(s->pev[j], s->stream) != cudaSuccess)
+          rc = fail(LRQ_ERUNTIME, "cudaEventRecord failed");
+      }
+      if (rc) return rc;
+    } else {
+      rc = w.prog == 1 ? launch_wd(s, gr.kind, w.kind, sp)
+           : fuse      ? (s->pbytes == 8 ? launch_sweep_kind<float>(s->stream, gr.kind, w.kind, sp, grid,
+                                                                     sweep_smem_bytes(nl, true, false, false))
+                                         : launch_sweep_kind<double>(s->stream, gr.kind, w.kind, sp, grid,
+                                                                      sweep_smem_bytes(nl, true, false, false)))
+                       : launch_sweep(s, gr.kind, w.kind, sp, grid);
+    }
     if (rc) return rc;
     record(s, ev++, "PMFRLQN"[w.kind]);
     if (fuse) {
@@ -840,8 +1107,12 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
       s->cur = 1 - s->cur;
       s->amps = s->bufs[s->cur];
       record(s, ev++, 'Y');
+    } else if (pipe) {
+      rc = remap_exchange(s, true, -1);
+      if (rc) return rc;
+      record(s, ev++, 'W');
     } else if (w.remap_after) {
-      rc = exchange_blocks(s, -1);
+      rc = remap_exchange(s, false, -1);
       if (rc) return rc;
       record(s, ev++, 'T');
     }
@@ -851,7 +1122,10 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
     if (rc) return rc;
   }
   record(s, ev++, 'Z');
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  {
+    const int rc = dist_wait(s, s->stream);
+    if (rc) return rc;
+  }
   if (s->timing) {
     s->last_ms.clear();
     for (size_t i = 1; i < ev; ++i) {
@@ -870,12 +1144,12 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
 int gather_out(lrq_state* s, std::vector<double>& h) {
   if (s->group) {
     lrq_group* G = s->group;
-    double mine[4];
+    double mine[kOutScalars];
     CUDA_TRY(cudaMemcpyAsync(mine, s->out, sizeof mine, cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     {
       std::lock_guard<std::mutex> lk(G->mu);
-      memcpy(&G->gather[4 * s->rank], mine, sizeof mine);
+      memcpy(&G->gather[kOutScalars * s->rank], mine, sizeof mine);
     }
     int rc = group_barrier(G);
     if (rc) return rc;
@@ -885,11 +1159,11 @@ int gather_out(lrq_state* s, std::vector<double>& h) {
     }
     return group_barrier(G);  // nobody overwrites a slot before all have read
   }
-  NCCL_TRY(nccl().AllGather(s->out, s->dgather, 4, ncclDouble, s->comm, s->stream));
-  h.resize(4 * s->world);
+  if (!s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
+  NCCL_TRY_S(s, nccl().AllGather(s->out, s->dgather, kOutScalars, ncclDouble, s->comm, s->stream));
+  h.resize(kOutScalars * s->world);
   CUDA_TRY(cudaMemcpyAsync(h.data(), s->dgather, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return LRQ_OK;
+  return dist_wait(s, s->stream);
 }
 
 }  // namespace
@@ -954,6 +1228,35 @@ int lrq_device_count(int* count) {
   return LRQ_OK;
 }
 
+int lrq_describe_remap(int world, int rank, int mirror, char* buf, size_t cap) {
+  if (world < 2 || (world & (world - 1))) return fail(LRQ_EVALIDATION, "world size must be a power of two >= 2");
+  if (rank < 0 || rank >= world || mirror >= world) return fail(LRQ_EVALIDATION, "rank out of range");
+  std::string js = "[";
+  const std::vector<RemapStep> v = remap_schedule(world, rank, mirror);
+  for (size_t i = 0; i < v.size(); ++i)
+    js += (i ? "," : "") + std::string("[") + std::to_string(v[i].partner) + "," + std::to_string(v[i].my_block) +
+          "," + std::to_string(v[i].their_block) + "," + std::to_string(v[i].half) + "]";
+  js += "]";
+  if (!buf || cap < js.size() + 1) return fail(LRQ_EVALIDATION, "buffer too small: need " + std::to_string(js.size() + 1));
+  memcpy(buf, js.c_str(), js.size() + 1);
+  return LRQ_OK;
+}
+
+int lrq_describe_memory(int n, int pbytes, int world, int p, uint64_t* state_bytes, uint64_t* other_bytes,
+                        uint64_t* extra_spare) {
+  if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
+  if (world < 1 || (world & (world - 1))) return fail(LRQ_EVALIDATION, "world size must be a power of two");
+  int g = 0;
+  while ((1 << g) < world) ++g;
+  if (n - g < 1 || n - g > 40) return fail(LRQ_EVALIDATION, "qubits per rank out of range [1, 40]");
+  const int nl = n - g;
+  const uint64_t st = (uint64_t)pbytes << nl;
+  if (state_bytes) *state_bytes = st;
+  if (other_bytes) *other_bytes = rank_extra_bytes(nl, pbytes, world, p, world > 1);
+  if (extra_spare) *extra_spare = world > 1 ? st : 0;
+  return LRQ_OK;
+}
+
 int lrq_describe_plan(int n, int pbytes, int p, char* buf, size_t cap) {
   if (pbytes != 8 && pbytes != 16) return fail(LRQ_EVALIDATION, "precision_bytes must be 8 or 16");
   if (n < 1 || n > 40) return fail(LRQ_EVALIDATION, "num_qubits out of range [1, 40]");
@@ -996,10 +1299,10 @@ int lrq_create(int n, int pbytes, int device, uint64_t budget, lrq_state** out) 
   s->num_tiles = n >= s->K ? (1ll << (n - s->K)) : 1;
   cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&s->amps, need);
-  if (e == cudaSuccess) e = cudaMalloc(&s->red, sizeof(double) * 4 * s->num_tiles);
+  if (e == cudaSuccess) e = cudaMalloc(&s->red, sizeof(double) * kRedArrays * s->num_tiles);
   if (e == cudaSuccess) e = cudaMalloc(&s->prefix, sizeof(double) * (s->num_tiles + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&s->out, sizeof(double) * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&s->fin, sizeof(double) * 5 * kFinBlocks);
+  if (e == cudaSuccess) e = cudaMalloc(&s->out, sizeof(double) * kOutScalars);
+  if (e == cudaSuccess) e = cudaMalloc(&s->fin, sizeof(double) * kFinScratch);
   // zero-fills on the engine's own (non-blocking) stream and waited for: a
   // legacy-stream cudaMemset is not ordered with it and could land after the
   // first lrq_set_cost copy
@@ -1045,26 +1348,19 @@ int create_rank_state(int n_total, int pbytes, int device, int rank, int world, 
   s->n_total = n_total;
   DeviceGuard guard(device);
   const size_t block = (size_t)pbytes << (nl - g);
-  s->chunk = block < (64ull << 20) ? block : (64ull << 20);
-  cudaError_t e = staging ? cudaMalloc(&s->stage, s->chunk * (size_t)(world - 1)) : cudaSuccess;
+  s->chunk = remap_chunk(block);
+  s->bufs[0] = s->amps;  // the primary buffer; a fused-remap spare comes later (group_prepare / lrq_ipc_handles)
+  cudaError_t e = staging ? cudaMalloc(&s->stage, s->chunk) : cudaSuccess;
   if (e == cudaSuccess) e = cudaMalloc(&s->dWx, sizeof(double) * nl);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->dWx, 0, sizeof(double) * nl, s->stream);
-  if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * 4 * world);
-  if (e == cudaSuccess) e = cudaMalloc(&s->dflag, sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * kOutScalars * world);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dflag, 2 * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->dflag, 0, 2 * sizeof(float), s->stream);
+  if (e == cudaSuccess) e = cudaMalloc(&s->probe, sizeof(float) * world);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) {
     free_state(s);
     return fail(LRQ_ECAPACITY, std::string("distributed buffers: ") + cudaGetErrorString(e));
-  }
-  // second state buffer for the fused remap, if it fits (else NCCL/swap remaps)
-  if (world <= 8 && env_int("LRQ_FUSED_REMAP", 1)) {
-    void* alt = nullptr;
-    if (cudaMalloc(&alt, s->state_bytes) == cudaSuccess) {
-      s->bufs[0] = s->amps;
-      s->bufs[1] = alt;
-    } else {
-      cudaGetLastError();
-    }
   }
   *out = s;
   return LRQ_OK;
@@ -1095,90 +1391,150 @@ int lrq_create_dist(int n_total, int pbytes, int device, int rank, int world, co
 
 int lrq_ipc_handles(lrq_state* s, void* out, size_t cap) {
   if (!s || !out) return fail(LRQ_EVALIDATION, "null argument");
-  if (cap < 2 * sizeof(cudaIpcMemHandle_t)) return fail(LRQ_EVALIDATION, "handle buffer too small");
-  memset(out, 0, 2 * sizeof(cudaIpcMemHandle_t));
-  if (!s->bufs[1]) return LRQ_OK;  // no second buffer: zero handles, fused remap stays off
+  if (cap < LRQ_IPC_HANDLE_BYTES) return fail(LRQ_EVALIDATION, "handle buffer too small");
+  memset(out, 0, LRQ_IPC_HANDLE_BYTES);
+  // zero handles: NCCL transport only ($LRQ_PEER_REMAP=0 forces it)
+  if (s->world < 2 || s->world > 8 || s->group || !env_int("LRQ_PEER_REMAP", 1)) return LRQ_OK;
   DeviceGuard guard(s->device);
-  cudaIpcMemHandle_t h[2];
+  // the fused remap's spare state buffer, only if it fits with 2 GiB to spare
+  // (lrq_fused_setup frees it again unless every rank got one)
+  if (!s->bufs[1] && env_int("LRQ_FUSED_REMAP", 1)) {
+    size_t freeb = 0, totalb = 0;
+    if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess && freeb >= s->state_bytes + (2ull << 30)) {
+      void* alt = nullptr;
+      if (cudaMalloc(&alt, s->state_bytes) == cudaSuccess) s->bufs[1] = alt;
+    }
+    cudaGetLastError();
+  }
+  cudaIpcMemHandle_t h[3];
+  memset(h, 0, sizeof h);
   CUDA_TRY(cudaIpcGetMemHandle(&h[0], s->bufs[0]));
-  CUDA_TRY(cudaIpcGetMemHandle(&h[1], s->bufs[1]));
+  if (s->bufs[1]) CUDA_TRY(cudaIpcGetMemHandle(&h[1], s->bufs[1]));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[2], s->probe));
   memcpy(out, h, sizeof h);
   return LRQ_OK;
 }
 
-// peer writes of the fused-remap self-test: rank writes (rank + 1) at the head
-// of its block in every rank's second buffer
-__global__ void fused_probe_kernel(void* const* dst, int world, int rank, size_t block_bytes) {
+// peer writes of the remap self-test: rank writes (rank + 1) into slot `rank`
+// of every rank's probe buffer
+__global__ void peer_probe_kernel(float* const* dst, int world, int rank) {
   const int b = threadIdx.x;
-  if (b < world) *reinterpret_cast<double*>((char*)dst[b] + (size_t)rank * block_bytes) = (double)(rank + 1);
+  if (b < world) dst[b][rank] = (float)(rank + 1);
 }
 
 int lrq_fused_setup(lrq_state* s, const void* all_handles, int* enabled) {
   if (!s || !all_handles || !enabled) return fail(LRQ_EVALIDATION, "null argument");
   *enabled = 0;
   if (s->world < 2 || s->group) return fail(LRQ_EVALIDATION, "lrq_fused_setup is for NCCL ranks");
+  if (!s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
   DeviceGuard guard(s->device);
-  const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(all_handles);
+  const int W = s->world;
   static const cudaIpcMemHandle_t zero = {};
-  bool ok = s->bufs[1] != nullptr;
-  for (int b = 0; b < s->world && ok; ++b) {
-    for (int i = 0; i < 2 && ok; ++i) {
-      if (b == s->rank) {
-        s->peer[i][b] = s->bufs[i];
-        continue;
-      }
-      if (!memcmp(&h[2 * b + i], &zero, sizeof zero)) {
-        ok = false;
-        break;
-      }
-      void* p = nullptr;
-      if (cudaIpcOpenMemHandle(&p, h[2 * b + i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
-        ok = false;
-        break;
-      }
-      s->ipc_open.push_back(p);
-      s->peer[i][b] = p;
+  auto handle = [&](int b, int i) {
+    return reinterpret_cast<const cudaIpcMemHandle_t*>(static_cast<const unsigned char*>(all_handles) +
+                                                       (size_t)b * LRQ_IPC_HANDLE_BYTES)[i];
+  };
+  // map the peers' primary buffers and probes (and spare buffers if all have one)
+  bool peer = W <= 8, spare = W <= 8;
+  std::vector<float*> probes(W, nullptr);
+  for (int b = 0; b < W && peer; ++b) {
+    if (b == s->rank) {
+      s->peer[0][b] = s->bufs[0];
+      s->peer[1][b] = s->bufs[1];
+      probes[b] = s->probe;
+      spare = spare && s->bufs[1];
+      continue;
     }
+    const cudaIpcMemHandle_t h0 = handle(b, 0), h1 = handle(b, 1), h2 = handle(b, 2);
+    if (!memcmp(&h0, &zero, sizeof zero) || !memcmp(&h2, &zero, sizeof zero)) {
+      peer = false;
+      break;
+    }
+    void* p0 = nullptr;
+    void* p2 = nullptr;
+    if (cudaIpcOpenMemHandle(&p0, h0, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&p2, h2, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      if (p0) cudaIpcCloseMemHandle(p0);
+      peer = false;
+      break;
+    }
+    s->ipc_open.push_back(p0);
+    s->ipc_open.push_back(p2);
+    s->peer[0][b] = p0;
+    probes[b] = reinterpret_cast<float*>(p2);
+    spare = spare && memcmp(&h1, &zero, sizeof zero) != 0;
   }
-  // collective self-test of the peer stores (every rank takes part even if
-  // its own mapping failed, so the collectives stay matched)
-  const size_t block = (size_t)s->pbytes << (s->n - s->g);
-  void** dptr = nullptr;
-  double* dv = nullptr;
-  CUDA_TRY(cudaMalloc(&dptr, sizeof(void*) * 8));
-  CUDA_TRY(cudaMalloc(&dv, sizeof(double) * 8));
-  std::vector<void*> dst(8, nullptr);
-  const int nxt = 1 - s->cur;  // probe the buffer that does not hold the state
-  for (int b = 0; b < s->world; ++b) dst[b] = ok ? s->peer[nxt][b] : nullptr;
-  CUDA_TRY(cudaMemcpyAsync(dptr, dst.data(), sizeof(void*) * 8, cudaMemcpyHostToDevice, s->stream));
-  if (ok) {
-    fused_probe_kernel<<<1, 32, 0, s->stream>>>(dptr, s->world, s->rank, block);
+  spare = spare && peer && s->bufs[1];
+  std::vector<void*> spares;
+  for (int b = 0; b < W && spare; ++b) {
+    if (b == s->rank) continue;
+    void* p1 = nullptr;
+    if (cudaIpcOpenMemHandle(&p1, handle(b, 1), cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      spare = false;
+      break;
+    }
+    spares.push_back(p1);
+    s->peer[1][b] = p1;
+  }
+  // collective self-test of the peer stores (every rank takes part even if its
+  // own mapping failed, so the collectives stay matched)
+  float** dptr = nullptr;
+  float* dv = nullptr;
+  CUDA_TRY(cudaMalloc(&dptr, sizeof(float*) * W));
+  CUDA_TRY(cudaMalloc(&dv, 2 * sizeof(float)));
+  CUDA_TRY(cudaMemsetAsync(s->probe, 0, sizeof(float) * W, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(dptr, probes.data(), sizeof(float*) * W, cudaMemcpyHostToDevice, s->stream));
+  int rc = dist_wait(s, s->stream);
+  if (rc) return rc;
+  NCCL_TRY_S(s, nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));  // probes zeroed
+  if (peer) {
+    peer_probe_kernel<<<1, 32, 0, s->stream>>>(dptr, W, s->rank);
     CUDA_TRY(cudaGetLastError());
   }
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  NCCL_TRY(nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));  // barrier
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  float good = 1.0f;
-  if (ok) {
-    for (int b = 0; b < s->world; ++b) {
-      double v = 0.0;
-      CUDA_TRY(cudaMemcpy(&v, (char*)s->bufs[nxt] + (size_t)b * block, sizeof v, cudaMemcpyDeviceToHost));
-      if (v != (double)(b + 1)) good = 0.0f;
-    }
-  } else {
-    good = 0.0f;
+  NCCL_TRY_S(s, nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));  // probes written
+  if ((rc = dist_wait(s, s->stream))) return rc;
+  float good[2] = {peer ? 1.0f : 0.0f, spare ? 1.0f : 0.0f};
+  if (peer) {
+    std::vector<float> got(W);
+    CUDA_TRY(cudaMemcpy(got.data(), s->probe, sizeof(float) * W, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < W; ++b)
+      if (got[b] != (float)(b + 1)) good[0] = good[1] = 0.0f;
   }
   // enabled only if every rank passed: minimum over ranks
-  float* dgood = reinterpret_cast<float*>(dv);
-  CUDA_TRY(cudaMemcpy(dgood, &good, sizeof good, cudaMemcpyHostToDevice));
-  NCCL_TRY(nccl().AllReduce(dgood, dgood, 1, ncclFloat, ncclMin, s->comm, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  CUDA_TRY(cudaMemcpy(&good, dgood, sizeof good, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(dv, good, sizeof good, cudaMemcpyHostToDevice));
+  NCCL_TRY_S(s, nccl().AllReduce(dv, dv, 2, ncclFloat, ncclMin, s->comm, s->stream));
+  if ((rc = dist_wait(s, s->stream))) return rc;
+  CUDA_TRY(cudaMemcpy(good, dv, sizeof good, cudaMemcpyDeviceToHost));
   cudaFree(dptr);
   cudaFree(dv);
-  s->fused = good == 1.0f;
-  *enabled = s->fused ? 1 : 0;
+  s->peer_ok = good[0] == 1.0f;
+  s->fused = s->peer_ok && good[1] == 1.0f;
+  if (!s->fused) {
+    // no fused remap anywhere: drop the spare buffer and the peers' mappings of theirs
+    for (void* q : spares) cudaIpcCloseMemHandle(q);
+    for (int b = 0; b < 8; ++b) s->peer[1][b] = nullptr;
+    if (s->bufs[1]) {
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+      // every rank has closed its mapping of our spare before we free it
+      NCCL_TRY_S(s, nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));
+      if ((rc = dist_wait(s, s->stream))) return rc;
+      if (s->cur == 1) {
+        CUDA_TRY(cudaMemcpy(s->bufs[0], s->bufs[1], s->state_bytes, cudaMemcpyDeviceToDevice));
+        s->cur = 0;
+        s->amps = s->bufs[0];
+      }
+      cudaFree(s->bufs[1]);
+      s->bufs[1] = nullptr;
+    } else {
+      NCCL_TRY_S(s, nccl().AllReduce(s->dflag, s->dflag, 1, ncclFloat, ncclSum, s->comm, s->stream));
+      if ((rc = dist_wait(s, s->stream))) return rc;
+    }
+  } else {
+    for (void* q : spares) s->ipc_open.push_back(q);
+  }
+  *enabled = s->fused ? 1 : (s->peer_ok ? 2 : 0);
   return LRQ_OK;
 }
 
@@ -1189,7 +1545,7 @@ int lrq_group_create(int world, lrq_group** out) {
   lrq_group* G = new lrq_group;
   G->world = world;
   G->members.assign(world, nullptr);
-  G->gather.assign(4 * (size_t)world, 0.0);
+  G->gather.assign(kOutScalars * (size_t)world, 0.0);
   G->shot_bufs.assign(world, nullptr);
   *out = G;
   return LRQ_OK;
@@ -1337,6 +1693,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   double* rpe = rp + s->num_tiles;
   double* rmin = rpe + s->num_tiles;
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
+  double* rmax = rmin + 2 * s->num_tiles;
   const int min_bit = n - 1;
 
   if (n < s->K) {
@@ -1369,6 +1726,9 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
+    sp.red_maxE = rmax;
+    if (const int rh = zero_hist(s)) return rh;
+    set_hist(s, sp);
     int rc = launch_small_any(s->pbytes, sp, s->stream);
     if (rc) return rc;
     record(s, ev++, 'S');
@@ -1422,6 +1782,11 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.red_pE = rpe;
       sp.red_minE = rmin;
       sp.red_arg = rarg;
+      sp.red_maxE = rmax;
+      if (w.reduce) {
+        if (const int rh = zero_hist(s)) return rh;
+        set_hist(s, sp);
+      }
       int rc = w.prog == 1 ? launch_wd(s, g.kind, w.kind, sp) : launch_sweep(s, g.kind, w.kind, sp, grid);
       if (rc) return rc;
       record(s, ev++, "PMFRLQN"[w.kind]);
@@ -1676,6 +2041,7 @@ int lrq_recompute(lrq_state* s) {
   double* rpe = rp + s->num_tiles;
   double* rmin = rpe + s->num_tiles;
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
+  double* rmax = rmin + 2 * s->num_tiles;
   if (n < s->K) {
     SmallParams sp;
     memset(&sp, 0, sizeof sp);
@@ -1691,6 +2057,9 @@ int lrq_recompute(lrq_state* s) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
+    sp.red_maxE = rmax;
+    if (const int rh = zero_hist(s)) return rh;
+    set_hist(s, sp);
     int rc = launch_small_any(s->pbytes, sp, s->stream);
     if (rc) return rc;
   } else {
@@ -1714,6 +2083,9 @@ int lrq_recompute(lrq_state* s) {
     sp.red_pE = rpe;
     sp.red_minE = rmin;
     sp.red_arg = rarg;
+    sp.red_maxE = rmax;
+    if (const int rh = zero_hist(s)) return rh;
+    set_hist(s, sp);
     const int grid_cap = 2 * sm_count(s->device);
     int rc = launch_sweep(s, GK_A, SK_Q, sp, (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap));
     if (rc) return rc;
@@ -1732,7 +2104,7 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
   if (!s || !out) return fail(LRQ_EVALIDATION, "null argument");
   if (!s->reduced) return fail(LRQ_ERUNTIME, "no reductions: set a cost and run the circuit first");
   DeviceGuard guard(s->device);
-  double h[4];
+  double h[kOutScalars];
   if (s->world > 1) {
     // collective: every rank's scalars, combined in rank order (deterministic);
     // local argmin -> global index (rank bits on top, identity permutation)
@@ -1742,19 +2114,21 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
       if (s->group) group_abort(s->group, g_err);
       return rc;
     }
-    double sp = 0.0, spe = 0.0, mn = __builtin_inf();
+    double sp = 0.0, spe = 0.0, mn = __builtin_inf(), mx = -__builtin_inf();
     uint64_t best = ~0ull;
     s->rank_sum_p.assign(s->world, 0.0);
     for (int r = 0; r < s->world; ++r) {
-      sp += all[4 * r];
-      spe += all[4 * r + 1];
-      s->rank_sum_p[r] = all[4 * r];
+      const double* a = &all[kOutScalars * r];
+      sp += a[0];
+      spe += a[1];
+      s->rank_sum_p[r] = a[0];
+      mx = fmax(mx, a[4]);
       uint64_t z;
-      memcpy(&z, &all[4 * r + 3], 8);
+      memcpy(&z, &a[3], 8);
       if (z == ~0ull) continue;
       const uint64_t gz = ((uint64_t)r << s->n) | z;
-      if (all[4 * r + 2] < mn || (all[4 * r + 2] == mn && gz < best)) {
-        mn = all[4 * r + 2];
+      if (a[2] < mn || (a[2] == mn && gz < best)) {
+        mn = a[2];
         best = gz;
       }
     }
@@ -1762,6 +2136,7 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
     out->sum_p_cut = 0.5 * (s->wtot * sp - spe);
     out->min_energy = mn;
     out->argmax_cut = best;
+    out->max_energy = mx;
     return LRQ_OK;
   }
   CUDA_TRY(cudaMemcpyAsync(h, s->out, sizeof h, cudaMemcpyDeviceToHost, s->stream));
@@ -1772,6 +2147,7 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
   uint64_t z;
   memcpy(&z, &h[3], 8);
   out->argmax_cut = z;
+  out->max_energy = h[4];
   return LRQ_OK;
 }
 
@@ -1821,10 +2197,17 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
     sample_kernel<double><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
                                                                     shots, off, total, base_index, s->didx);
   CUDA_TRY(cudaGetLastError());
-  if (s->world > 1 && !s->group)  // exactly one rank owns each shot; the others wrote 0
-    NCCL_TRY(nccl().AllReduce(s->didx, s->didx, shots, ncclUint64, ncclSum, s->comm, s->stream));
+  if (s->world > 1 && !s->group) {  // exactly one rank owns each shot; the others wrote 0
+    if (!s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
+    NCCL_TRY_S(s, nccl().AllReduce(s->didx, s->didx, shots, ncclUint64, ncclSum, s->comm, s->stream));
+  }
   CUDA_TRY(cudaMemcpyAsync(idx, s->didx, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->world > 1 && !s->group) {
+    const int rc = dist_wait(s, s->stream);
+    if (rc) return rc;
+  } else {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
   if (s->group) {
     const int rc = group_sum_shots(s, idx, shots);
     if (rc) group_abort(s->group, g_err);
@@ -1890,6 +2273,146 @@ int lrq_cut_values(int n, const double* w, const uint64_t* z, uint64_t start, in
   return LRQ_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// one-shot device scratch of the host-array entry points below: a stream and
+// the buffers, freed on every path
+struct Scratch {
+  int device;
+  cudaStream_t st = nullptr;
+  std::vector<void*> bufs;
+  explicit Scratch(int d) : device(d) {}
+  cudaError_t init() { return cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking); }
+  template <typename P>
+  cudaError_t alloc(P** p, size_t bytes) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, bytes ? bytes : 8);
+    if (e == cudaSuccess) bufs.push_back(q);
+    *p = reinterpret_cast<P*>(q);
+    return e;
+  }
+  ~Scratch() {
+    if (st) cudaStreamSynchronize(st);
+    for (void* q : bufs) cudaFree(q);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+int need_device(const char* what) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LRQ_ERUNTIME, std::string("no CUDA device available (") + what + " has no CPU path)");
+  return LRQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int lrq_cut_values_spin(int n, const double* w, double half_total, uint64_t start, int64_t count, double* out,
+                        int device) {
+  if (n < 2 || n > 63) return fail(LRQ_EVALIDATION, "num_qubits out of range [2, 63]");
+  if (!w || !out || count < 0) return fail(LRQ_EVALIDATION, "null argument");
+  if (count == 0) return LRQ_OK;
+  if (int rc = need_device("cut values")) return rc;
+  DeviceGuard guard(device);
+  std::vector<double> A((size_t)n * n);
+  sym_matrix(n, w, A.data());
+  Scratch sc(device);
+  double *dA = nullptr, *dout = nullptr;
+  cudaError_t e = sc.init();
+  if (e == cudaSuccess) e = sc.alloc(&dA, sizeof(double) * n * n);
+  const int64_t step = 1ll << 26;
+  if (e == cudaSuccess) e = sc.alloc(&dout, sizeof(double) * (count < step ? count : step));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, sc.st);
+  for (int64_t off = 0; e == cudaSuccess && off < count; off += step) {
+    const int64_t m = count - off < step ? count - off : step;
+    const long long blocks = (m + 255) / 256;
+    cut_values_spin_kernel<<<(unsigned)(blocks < 65535 ? blocks : 65535), 256, sizeof(double) * n * n, sc.st>>>(
+        n, dA, half_total, (unsigned long long)(start + off), m, dout);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out + off, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, sc.st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st);
+  }
+  CUDA_TRY(e);
+  return LRQ_OK;
+}
+
+int lrq_expected_cut(int n, const double* w, double half_total, const double* probs, uint64_t count,
+                     double* chunk_sums, int device) {
+  if (n < 2 || n > 40) return fail(LRQ_EVALIDATION, "num_qubits out of range [2, 40]");
+  if (!w || !probs || !chunk_sums) return fail(LRQ_EVALIDATION, "null argument");
+  if (count != (1ull << n)) return fail(LRQ_EVALIDATION, "distribution size must be 2^n");
+  if (int rc = need_device("expected cut")) return rc;
+  DeviceGuard guard(device);
+  const int cb = n < 16 ? n : 16;  // reference chunk: 2^16 (engine.py:29)
+  const long long chunks = (long long)(count >> cb);
+  std::vector<double> A((size_t)n * n);
+  sym_matrix(n, w, A.data());
+  Scratch sc(device);
+  double *dA = nullptr, *dp = nullptr, *ds = nullptr;
+  cudaError_t e = sc.init();
+  if (e == cudaSuccess) e = sc.alloc(&dA, sizeof(double) * n * n);
+  if (e == cudaSuccess) e = sc.alloc(&dp, sizeof(double) * count);
+  if (e == cudaSuccess) e = sc.alloc(&ds, sizeof(double) * chunks);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, sc.st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dp, probs, sizeof(double) * count, cudaMemcpyHostToDevice, sc.st);
+  if (e == cudaSuccess) {
+    expected_cut_kernel<<<(unsigned)chunks, 256, sizeof(double) * n * n, sc.st>>>(n, dA, half_total, dp,
+                                                                                   (long long)count, cb, ds);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(chunk_sums, ds, sizeof(double) * chunks, cudaMemcpyDeviceToHost, sc.st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st);
+  CUDA_TRY(e);
+  return LRQ_OK;
+}
+
+int lrq_draw_indices(const double* probs, uint64_t count, const double* u, int64_t shots, uint64_t* idx_out,
+                     int device) {
+  if (!probs || !u || !idx_out) return fail(LRQ_EVALIDATION, "null argument");
+  if (shots < 1) return fail(LRQ_EVALIDATION, "shot count must be positive, got " + std::to_string(shots));
+  if (count < 1) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
+  if (int rc = need_device("draw_indices")) return rc;
+  DeviceGuard guard(device);
+  int tb = 0;
+  while (tb < 12 && (1ull << tb) < count) ++tb;
+  const long long T = (long long)((count + (1ull << tb) - 1) >> tb);
+  Scratch sc(device);
+  double *dp = nullptr, *red = nullptr, *prefix = nullptr, *out = nullptr, *fin = nullptr, *du = nullptr;
+  unsigned long long* didx = nullptr;
+  cudaError_t e = sc.init();
+  if (e == cudaSuccess) e = sc.alloc(&dp, sizeof(double) * count);
+  if (e == cudaSuccess) e = sc.alloc(&red, sizeof(double) * kRedArrays * T);
+  if (e == cudaSuccess) e = sc.alloc(&prefix, sizeof(double) * (T + 1));
+  if (e == cudaSuccess) e = sc.alloc(&out, sizeof(double) * kOutScalars);
+  if (e == cudaSuccess) e = sc.alloc(&fin, sizeof(double) * kFinScratch);
+  if (e == cudaSuccess) e = sc.alloc(&du, sizeof(double) * shots);
+  if (e == cudaSuccess) e = sc.alloc(&didx, sizeof(unsigned long long) * shots);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dp, probs, sizeof(double) * count, cudaMemcpyHostToDevice, sc.st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(du, u, sizeof(double) * shots, cudaMemcpyHostToDevice, sc.st);
+  // the finalize reads all four partial arrays: zero sums, +inf minima
+  if (e == cudaSuccess) e = cudaMemsetAsync(red + T, 0, sizeof(double) * T, sc.st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(red + 2 * T, 0x7f, sizeof(double) * T, sc.st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(red + 3 * T, 0xff, sizeof(double) * T, sc.st);
+  if (e == cudaSuccess) {
+    prob_tile_sums_kernel<<<(unsigned)((T * 32 + 255) / 256), 256, 0, sc.st>>>(dp, (long long)count, tb, T, red);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && launch_finalize(sc.st, T, red, prefix, out, fin) != LRQ_OK) e = cudaErrorUnknown;
+  double total = 0.0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&total, out, sizeof(double), cudaMemcpyDeviceToHost, sc.st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sc.st);
+  CUDA_TRY(e);
+  if (!(total > 0.0)) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
+  sample_probs_kernel<<<(unsigned)((shots * 32 + 255) / 256), 256, 0, sc.st>>>(dp, (long long)count, tb, T, prefix,
+                                                                                du, shots, didx);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(idx_out, didx, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, sc.st));
+  CUDA_TRY(cudaStreamSynchronize(sc.st));
+  return LRQ_OK;
+}
+
 int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* value) {
   if (n < 2 || n > 48) return fail(LRQ_EVALIDATION, "num_qubits out of range [2, 48]");
   if (!w || !argmax || !value) return fail(LRQ_EVALIDATION, "null argument");
@@ -1921,6 +2444,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
       sp.red_pE = rp + 1;
       sp.red_minE = rp + 2;
       sp.red_arg = reinterpret_cast<unsigned long long*>(rp + 3);
+      sp.red_maxE = rp + 4;
       rc = launch_small_any(16, sp, s->stream);
       cudaError_t e = rc ? cudaErrorUnknown : cudaSuccess;
       if (e == cudaSuccess) e = cudaMemcpyAsync(&best, rp + 3, 8, cudaMemcpyDeviceToHost, s->stream);
@@ -1939,11 +2463,11 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
     std::vector<double> M((size_t)n * n);
     sym_matrix(n, w, M.data());
     cudaError_t e = cudaMalloc(&dW, sizeof(double) * n * n);
-    if (e == cudaSuccess) e = cudaMalloc(&red, sizeof(double) * 4 * T);
+    if (e == cudaSuccess) e = cudaMalloc(&red, sizeof(double) * kRedArrays * T);
     if (e == cudaSuccess) e = cudaMalloc(&prefix, sizeof(double) * (T + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(double) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(double) * kOutScalars);
     if (e == cudaSuccess) e = cudaMalloc(&zero, sizeof(double) * (n + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&fin, sizeof(double) * 5 * kFinBlocks);
+    if (e == cudaSuccess) e = cudaMalloc(&fin, sizeof(double) * kFinScratch);
     if (e == cudaSuccess) e = cudaMemsetAsync(zero, 0, sizeof(double) * (n + 1), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(red, 0, sizeof(double) * 2 * T, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dW, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, st);
@@ -1964,6 +2488,7 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
       sp.red_pE = red + T;
       sp.red_minE = red + 2 * T;
       sp.red_arg = reinterpret_cast<unsigned long long*>(red + 3 * T);
+      sp.red_maxE = red + 4 * T;
       const int grid_cap = 2 * sm_count(device);
       const int grid = (int)(T < grid_cap ? T : grid_cap);
       const size_t smem = sweep_smem_bytes(n, false, false, true);
@@ -1985,6 +2510,65 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
   }
   *argmax = best;
   return lrq_cut_values(n, w, &best, 0, 1, value, device);
+}
+
+int lrq_set_histogram(lrq_state* s, int bins, double lo, double hi) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (bins < 0 || bins > 4096) return fail(LRQ_EVALIDATION, "histogram bins must be in [0, 4096]");
+  if (bins && !(isfinite(lo) && isfinite(hi) && hi > lo)) return fail(LRQ_EVALIDATION, "histogram range must be finite, hi > lo");
+  DeviceGuard guard(s->device);
+  if (bins != s->hist_bins) {
+    cudaFree(s->dhist);
+    s->dhist = nullptr;
+    s->hist_bins = 0;
+    if (bins) {
+      CUDA_TRY(cudaMalloc(&s->dhist, sizeof(unsigned long long) * bins));
+      CUDA_TRY(cudaMemsetAsync(s->dhist, 0, sizeof(unsigned long long) * bins, s->stream));
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+  }
+  s->hist_bins = bins;
+  s->hist_lo = lo;
+  s->hist_hi = hi;
+  s->reduced = false;  // the next reducing pass fills it
+  return LRQ_OK;
+}
+
+int lrq_get_histogram(lrq_state* s, uint64_t* raw) {
+  if (!s || !raw) return fail(LRQ_EVALIDATION, "null argument");
+  if (!s->dhist) return fail(LRQ_ERUNTIME, "no histogram: call lrq_set_histogram, then run or recompute");
+  if (!s->reduced) return fail(LRQ_ERUNTIME, "no reductions: run the circuit or recompute first");
+  DeviceGuard guard(s->device);
+  const int B = s->hist_bins;
+  if (s->world > 1 && !s->group) {
+    if (!s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
+    // integer sums: the same result in any reduction order; afterwards every
+    // rank holds the total (until the next reducing pass re-zeroes it)
+    if (!s->hist_summed)
+      NCCL_TRY_S(s, nccl().AllReduce(s->dhist, s->dhist, B, ncclUint64, ncclSum, s->comm, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(raw, s->dhist, sizeof(uint64_t) * B, cudaMemcpyDeviceToHost, s->stream));
+    const int rc = dist_wait(s, s->stream);
+    s->hist_summed = rc == LRQ_OK;
+    return rc;
+  }
+  CUDA_TRY(cudaMemcpyAsync(raw, s->dhist, sizeof(uint64_t) * B, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->group) {
+    lrq_group* G = s->group;
+    {
+      std::lock_guard<std::mutex> lk(G->mu);
+      G->shot_bufs[s->rank] = raw;
+    }
+    int rc = group_barrier(G);
+    if (rc) return rc;
+    std::vector<uint64_t> sum((size_t)B, 0);
+    for (int r = 0; r < G->world; ++r)
+      for (int b = 0; b < B; ++b) sum[b] += G->shot_bufs[r][b];
+    rc = group_barrier(G);
+    if (rc) return rc;
+    memcpy(raw, sum.data(), sizeof(uint64_t) * B);
+  }
+  return LRQ_OK;
 }
 
 int lrq_set_timing(lrq_state* s, int enable) {

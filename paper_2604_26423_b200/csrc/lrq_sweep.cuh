@@ -143,6 +143,14 @@ struct SweepParams {
   double* red_pE;
   double* red_minE;
   unsigned long long* red_arg;
+  double* red_maxE;  // per-tile max E (may be null)
+  // p-weighted energy histogram (may be null): bin b = floor((E - hist_lo) *
+  // hist_scale) clamped to [0, hist_bins); each amplitude adds round(p 2^60)
+  // to its bin as a 64-bit integer, so the totals do not depend on the order
+  // (deterministic) and sum to 2^60 sum p
+  unsigned long long* hist;
+  int hist_bins;
+  double hist_lo, hist_scale;
   // fused remap (distributed plans, group-A M sweep before a remap): the tiles
   // of block b (top g local bits; 2^rbits tiles each) are stored straight
   // into rdst[b], rank b's next state buffer at this rank's block (peer
@@ -157,7 +165,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 constexpr int kTileUnitsPadded = (1 << kUnitBits) + (1 << (kUnitBits - 4));
 
 // dynamic shared memory of sweep_kernel
-__host__ __device__ inline size_t sweep_smem_bytes(int n, bool amps, bool usesJ, bool usesW) {
+__host__ __device__ inline size_t sweep_smem_bytes(int n, bool amps, bool usesJ, bool usesW, int hist_bins = 0) {
   size_t b = amps ? 16 * (size_t)kTileUnitsPadded : 0;
   if (usesJ) b = align16(b + 8 * (size_t)(n * n + n));
   if (usesW) b = align16(b + 8 * (size_t)(n * n + n));
@@ -165,9 +173,11 @@ __host__ __device__ inline size_t sweep_smem_bytes(int n, bool amps, bool usesJ,
   b += 8 * (size_t)(2 * 6 * kThreads);  // per-thread constants [mat][RA+1][thread]
   b = align16(b);
   b += 16 * 32 + 8 * 32 + 8 * 32;  // PRR[32] (c128), PRR32[32] (c64), ERR[32]
-  b += 8 * 4 * (kThreads / 32);  // reduction scratch
+  b += 8 * 5 * (kThreads / 32);  // reduction scratch
+  b += 8 * (size_t)hist_bins;     // shared energy histogram
   return align16(b);
 }
+
 
 template <typename T>
 struct UnitT;

@@ -32,6 +32,7 @@ struct SweepTile {
     const float2* PRR32;
     const double* ERR;
     double* rs;
+    unsigned long long* shist;  // shared energy histogram (null: off)
     uint64_t base;  // amp index of tile element 0
     long long tid;
     int t, q0, qU;
@@ -151,7 +152,9 @@ struct SweepTile {
       Ehi[h] = e;
     }
     double sp_ = 0.0, spe = 0.0, mine = __longlong_as_double(0x7ff0000000000000ll);
+    double maxe = -__longlong_as_double(0x7ff0000000000000ll);
     int bestv = NV;
+    unsigned long long* shist = c.shist;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const double ev = (Elo[v & 3] + Ehi[v >> 2]) + c.ERR[v];
@@ -159,7 +162,9 @@ struct SweepTile {
         const double pv = prob(amp_get(c.r, v));
         sp_ += pv;
         spe = fma(pv, ev, spe);
+        if (shist) hist_add(shist, P.hist_bins, P.hist_lo, P.hist_scale, ev, pv);
       }
+      maxe = fmax(maxe, ev);
       if (thread_ok && !(v & vmask) && ev < mine) {
         mine = ev;
         bestv = v;
@@ -180,32 +185,36 @@ struct SweepTile {
         mine = om;
         zbest = oz;
       }
+      maxe = fmax(maxe, __shfl_xor_sync(0xffffffffu, maxe, o));
     }
     const int warp = c.t >> 5;
     if ((c.t & 31) == 0) {
-      c.rs[warp * 4 + 0] = sp_;
-      c.rs[warp * 4 + 1] = spe;
-      c.rs[warp * 4 + 2] = mine;
-      c.rs[warp * 4 + 3] = __longlong_as_double((long long)zbest);
+      c.rs[warp * 5 + 0] = sp_;
+      c.rs[warp * 5 + 1] = spe;
+      c.rs[warp * 5 + 2] = mine;
+      c.rs[warp * 5 + 3] = __longlong_as_double((long long)zbest);
+      c.rs[warp * 5 + 4] = maxe;
     }
     team_sync(c.bar);  // the 256 threads of this team only
     if (c.t == 0) {
-      double s0 = 0.0, s1 = 0.0, mn = c.rs[2];
+      double s0 = 0.0, s1 = 0.0, mn = c.rs[2], mx = c.rs[4];
       unsigned long long zb = (unsigned long long)__double_as_longlong(c.rs[3]);
       for (int w = 0; w < kThreads / 32; ++w) {
-        s0 += c.rs[w * 4 + 0];
-        s1 += c.rs[w * 4 + 1];
-        const double om = c.rs[w * 4 + 2];
-        const unsigned long long oz = (unsigned long long)__double_as_longlong(c.rs[w * 4 + 3]);
+        s0 += c.rs[w * 5 + 0];
+        s1 += c.rs[w * 5 + 1];
+        const double om = c.rs[w * 5 + 2];
+        const unsigned long long oz = (unsigned long long)__double_as_longlong(c.rs[w * 5 + 3]);
         if (om < mn || (om == mn && oz < zb)) {
           mn = om;
           zb = oz;
         }
+        mx = fmax(mx, c.rs[w * 5 + 4]);
       }
       P.red_p[c.tid] = s0;
       P.red_pE[c.tid] = s1;
       P.red_minE[c.tid] = mn;
       P.red_arg[c.tid] = zb;
+      if (P.red_maxE) P.red_maxE[c.tid] = mx;
     }
   }
 
@@ -279,6 +288,10 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   float2* PRR32 = reinterpret_cast<float2*>(PRR + 32);
   double* ERR = reinterpret_cast<double*>(PRR32 + 32);
   double* rs = ERR + 32;
+  unsigned long long* shist = reinterpret_cast<unsigned long long*>(rs + 5 * (kThreads / 32));
+  const bool hist = HAS_REDUCE && AMPS && P.hist != nullptr;
+  if (hist)
+    for (int i = t; i < P.hist_bins; i += kThreads) shist[i] = 0ull;
 
   for (int i = t; i < n * n; i += kThreads) {
     if (HAS_PHASE) Jm[i] = P.J.M[i];
@@ -311,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   c.PRR32 = PRR32;
   c.ERR = ERR;
   c.rs = rs;
+  c.shist = hist ? shist : nullptr;
   c.t = t;
   c.q0 = q0;
   c.qU = qU;
@@ -392,6 +406,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
 #pragma unroll
       for (int j = 0; j < 16; ++j) st_unit(g + ((uint64_t)j << sh), c.r[j]);
     }
+  }
+  if (hist) {  // the CTA's histogram into the global one (integer adds: any order)
+    __syncthreads();
+    for (int i = t; i < P.hist_bins; i += kThreads)
+      if (shist[i]) atomicAdd(P.hist + i, shist[i]);
   }
 }
 

@@ -28,7 +28,7 @@ __host__ __device__ inline size_t tma_smem_bytes(int n, int nst, int teams, bool
   b += 8 * (size_t)(((usesJ ? 1 : 0) + (usesW ? 1 : 0)) * 6 * kThreads);  // per-thread constants (shared by teams)
   b = align16(b);
   b += 16 * 32 + 8 * 32 + 8 * 32;                                    // PRR, PRR32, ERR
-  b += (size_t)teams * 8 * (2 * 2 * 16 + 4 + 4 * (kThreads / 32));  // per team: hB, EBB, reduce scratch
+  b += (size_t)teams * 8 * (2 * 2 * 16 + 4 + 5 * (kThreads / 32));  // per team: hB, EBB, reduce scratch
   return align16(b) + 1024;  // slack for the 1024-byte stage alignment
 }
 
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(TEAMS* kThreads, 1) sweep_tma_kernel(const __g
   double2* PRR = reinterpret_cast<double2*>(sp);
   float2* PRR32 = reinterpret_cast<float2*>(PRR + 32);
   double* ERR = reinterpret_cast<double*>(PRR32 + 32);
-  double* teamb = ERR + 32 + team * (2 * 2 * 16 + 4 + 4 * (kThreads / 32));
+  double* teamb = ERR + 32 + team * (2 * 2 * 16 + 4 + 5 * (kThreads / 32));
   double* hB = teamb;
   double* EBB = hB + 2 * 2 * 16;
   double* rs = EBB + 4;
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(TEAMS* kThreads, 1) sweep_tma_kernel(const __g
   c.PRR32 = PRR32;
   c.ERR = ERR;
   c.rs = rs;
+  c.shist = nullptr;  // the histogram runs on the register path (launch_sweep)
   c.t = t;
   c.q0 = q0;
   c.qU = qU;

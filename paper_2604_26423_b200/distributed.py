@@ -73,6 +73,19 @@ class DistStateVector:
     def _draw(self, u: np.ndarray) -> np.ndarray:
         return self._dev.sample(u)
 
+    def _histogram(self, weights: np.ndarray, bins: int, lo: float, hi: float):
+        """Collective: one read-only pass with the E histogram on."""
+        self._dev.set_cost(weights)
+        self._dev.set_histogram(bins, lo, hi)
+        try:
+            self._dev.recompute()
+            raw = self._dev.histogram()
+            red = self._dev.reduce()
+        finally:
+            self._dev.set_histogram(0)
+        self._cost = np.array(weights, dtype=np.float64)
+        return raw, red
+
     def exact_expected_r(self, inst: WmcInstance) -> float:
         """Collective; same as engine.exact_expected_r(self, inst)."""
         if inst.num_vertices != self.num_qubits:
@@ -131,18 +144,28 @@ def drain_dist_pool() -> None:
         dev.close()
 
 
-def enable_fused_remap(dev: _native.DeviceState, group=None) -> bool:
-    """Collective: exchange the ranks' state-buffer handles and map them so
-    the sweep before each remap stores straight into peer memory
-    (lrq_fused_setup; falls back to the NCCL remap on every rank if any
-    rank cannot map or verify its peers)."""
+REMAP_MODES = {0: "nccl", 1: "fused", 2: "peer"}
+
+
+def enable_peer_remap(dev: _native.DeviceState, group=None) -> str:
+    """Collective: exchange the ranks' buffer handles and map them
+    (lrq_fused_setup).  Returns the remap transport every rank will use:
+    "fused" (a spare buffer fits: the sweep before a remap stores straight
+    into the owners' spares), "peer" (the state fills HBM: in-place pipelined
+    block swaps over NVLink) or "nccl" (no peer mapping: pipelined
+    send/recv)."""
     import torch.distributed as dist
 
     mine = dev.ipc_handles()
     world = dist.get_world_size(group)
     allh = [None] * world
     dist.all_gather_object(allh, mine, group=group)
-    return dev.fused_setup(b"".join(allh))
+    return REMAP_MODES[dev.fused_setup(b"".join(allh))]
+
+
+def enable_fused_remap(dev: _native.DeviceState, group=None) -> bool:
+    """Backward-compatible name: True when the fused form was enabled."""
+    return enable_peer_remap(dev, group) == "fused"
 
 
 def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Precision.FP32, group=None,
@@ -168,7 +191,7 @@ def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Pre
         dist.broadcast_object_list(box, src=0, group=group)
         dev = _native.DeviceState.create_dist(n, precision.bytes_per_amplitude, dev_index, rank, world, box[0],
                                               int(memory_budget or 0))
-        enable_fused_remap(dev, group)
+        dev.remap_mode = enable_peer_remap(dev, group)
     cost = getattr(circuit, "cost_weights", None)
     dev.set_cost(cost if cost is not None else np.zeros(n * (n - 1) // 2))
     dev.run(layers.phase, layers.mixer)

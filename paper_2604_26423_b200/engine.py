@@ -29,10 +29,11 @@ from .errors import CapacityError, StateError, ValidationError
 from .problem import WmcInstance, index_to_bitstring
 from .rng import derive_rng
 
-# The reference's default budget models host RAM (4 GiB).  The device state
-# is bounded by HBM instead: without an explicit budget or
-# LRQBENCH_MEMORY_BYTES the only limit is what the device can allocate.
-DEFAULT_MEMORY_BUDGET = None
+# The reference's default budget (engine.py:31): 4 GiB unless
+# LRQBENCH_MEMORY_BYTES or an explicit memory_budget says otherwise.  The
+# same contract holds here, so a drop-in user sees the same CapacityError;
+# large device states pass a budget (bench.py, the CLI's --memory-bytes).
+DEFAULT_MEMORY_BUDGET = 4 << 30
 
 
 class Precision(enum.Enum):
@@ -61,17 +62,16 @@ def state_bytes(num_qubits: int, precision: Precision) -> int:
     return precision.bytes_per_amplitude << num_qubits
 
 
-def memory_budget_bytes(override: int | None = None) -> int | None:
+def memory_budget_bytes(override: int | None = None) -> int:
     if override is not None:
         return int(override)
-    env = os.environ.get("LRQBENCH_MEMORY_BYTES")
-    return int(env) if env else DEFAULT_MEMORY_BUDGET
+    return int(os.environ.get("LRQBENCH_MEMORY_BYTES", DEFAULT_MEMORY_BUDGET))
 
 
 def check_memory(num_qubits: int, precision: Precision, budget: int | None = None) -> None:
     need = state_bytes(num_qubits, precision)
     limit = memory_budget_bytes(budget)
-    if limit is not None and need > limit:
+    if need > limit:
         raise CapacityError(
             f"statevector for {num_qubits} qubits at {precision.value} needs "
             f"{need} bytes ({need / (1 << 30):.1f} GiB), budget is {limit} bytes")
@@ -80,18 +80,39 @@ def check_memory(num_qubits: int, precision: Precision, budget: int | None = Non
 class StateVector:
     """A state vector resident in HBM (one ``lrq_state``).
 
-    ``amps`` performs an explicit device-to-host copy (cached) — only sensible
-    when 2^n amplitudes fit host memory.  Reductions (norm, exact r) and
-    sampling run on the device.
+    Two constructions: the reference's ``StateVector(num_qubits, amps)``
+    (engine.py:77-96) uploads a host array (complex64 stays FP32, anything
+    else becomes complex128 / FP64); the engine wraps a device state it made
+    (``StateVector._wrap``).  ``amps`` is an explicit device-to-host copy,
+    cached and read-only (a write to it would not reach the device, so it
+    raises instead of being dropped); gates and runs invalidate the cache.
+    Reductions (norm, exact r) and sampling run on the device.
     """
 
-    def __init__(self, num_qubits: int, precision: Precision, device_state: _native.DeviceState,
-                 cost_weights: np.ndarray | None = None):
-        self.num_qubits = num_qubits
-        self._precision = precision
-        self._dev = device_state
+    def __init__(self, num_qubits: int, amps=None, *, device_state: "_native.DeviceState | None" = None,
+                 precision: "Precision | None" = None, cost_weights: np.ndarray | None = None):
+        self.num_qubits = int(num_qubits)
         self._cost = None if cost_weights is None else np.asarray(cost_weights, dtype=np.float64)
         self._amps = None
+        if device_state is None:
+            if amps is None:
+                raise ValidationError("StateVector needs amplitudes (or a device state)")
+            a = np.asarray(amps)
+            a = a if a.dtype == np.complex64 else a.astype(np.complex128)
+            if a.ndim != 1 or a.size != 1 << self.num_qubits:
+                raise ValidationError(f"{a.size} amplitudes do not form a {self.num_qubits}-qubit state")
+            precision = Precision.FP32 if a.dtype == np.complex64 else Precision.FP64
+            device_state = _native.DeviceState(self.num_qubits, precision.bytes_per_amplitude)
+            device_state.store_amps(a)
+        elif precision is None:
+            precision = Precision.FP32 if device_state.precision_bytes == 8 else Precision.FP64
+        self._precision = precision
+        self._dev = device_state
+
+    @classmethod
+    def _wrap(cls, num_qubits: int, precision: Precision, device_state: "_native.DeviceState",
+              cost_weights: np.ndarray | None = None) -> "StateVector":
+        return cls(num_qubits, device_state=device_state, precision=precision, cost_weights=cost_weights)
 
     @property
     def precision(self) -> Precision:
@@ -99,38 +120,46 @@ class StateVector:
 
     @property
     def device_state(self) -> _native.DeviceState:
+        if self._dev is None:
+            raise StateError("state vector has been released")
         return self._dev
 
     @property
     def amps(self) -> np.ndarray:
         if self._amps is None:
-            self._amps = self._dev.copy_amps()
+            a = self.device_state.copy_amps()
+            a.setflags(write=False)
+            self._amps = a
         return self._amps
 
     def release(self) -> None:
-        """Free the device memory now (the handle is also freed on GC)."""
-        self._dev.close()
+        """Free the device memory now (cudaFree; not parked for reuse)."""
+        if self._dev is not None:
+            self._dev.close(park=False)
+            self._dev = None
+        self._amps = None
 
     def _reductions(self, weights: np.ndarray | None):
         """Final-pass reductions for cost ``weights`` (None: any cost)."""
+        dev = self.device_state
         if weights is not None and (self._cost is None or not np.array_equal(self._cost, weights)):
-            self._dev.set_cost(weights)
-            self._dev.recompute()
+            dev.set_cost(weights)
+            dev.recompute()
             self._cost = np.array(weights, dtype=np.float64)
         elif self._cost is None and weights is None:
             try:
-                return self._dev.reduce()
+                return dev.reduce()
             except StateError:
-                self._dev.recompute()
-        return self._dev.reduce()
+                dev.recompute()
+        return dev.reduce()
 
     def _copy_range(self, start: int, count: int) -> np.ndarray:
-        return self._dev.copy_amps(start, count)
+        return self.device_state.copy_amps(start, count)
 
     def _draw(self, u: np.ndarray) -> np.ndarray:
         """Global indices of the inverse-CDF draws for uniforms u."""
         self._reductions(None)
-        return self._dev.sample(u)
+        return self.device_state.sample(u)
 
     def norm_squared(self) -> float:
         return float(self._reductions(None).sum_p)
@@ -142,6 +171,20 @@ class StateVector:
     def probabilities(self) -> np.ndarray:
         a = self.amps.astype(np.complex128, copy=False)
         return (a.real ** 2 + a.imag ** 2).astype(np.float64)
+
+    def _histogram(self, weights: np.ndarray, bins: int, lo: float, hi: float):
+        """One read-only pass with the E histogram on: (raw bins, reductions)."""
+        dev = self.device_state
+        dev.set_cost(weights)
+        dev.set_histogram(bins, lo, hi)
+        try:
+            dev.recompute()
+            raw = dev.histogram()
+            red = dev.reduce()
+        finally:
+            dev.set_histogram(0)
+        self._cost = np.array(weights, dtype=np.float64)
+        return raw, red
 
 
 def _device_state(num_qubits: int, precision: Precision, memory_budget: int | None):
@@ -160,7 +203,7 @@ def zero_state(num_qubits: int, precision: Precision | str = Precision.FP32,
     precision = Precision.coerce(precision)
     dev = _device_state(num_qubits, precision, memory_budget)
     dev.reset(0)
-    return StateVector(num_qubits, precision, dev)
+    return StateVector._wrap(num_qubits, precision, dev)
 
 
 def init_plus_state(num_qubits: int, precision: Precision | str = Precision.FP32,
@@ -169,7 +212,7 @@ def init_plus_state(num_qubits: int, precision: Precision | str = Precision.FP32
     precision = Precision.coerce(precision)
     dev = _device_state(num_qubits, precision, memory_budget)
     dev.reset(1)
-    return StateVector(num_qubits, precision, dev)
+    return StateVector._wrap(num_qubits, precision, dev)
 
 
 def _touch(sv: StateVector) -> None:
@@ -177,26 +220,69 @@ def _touch(sv: StateVector) -> None:
     sv._cost = None
 
 
+def _check_qubit(sv: StateVector, q: int) -> None:
+    if not 0 <= q < sv.num_qubits:
+        raise ValidationError(f"qubit {q} out of range for {sv.num_qubits} qubits")
+
+
 def apply_h(sv: StateVector, q: int) -> None:
+    _check_qubit(sv, q)
     sv.device_state.apply_gate(0, q)
     _touch(sv)
 
 
 def apply_rx(sv: StateVector, theta: float, q: int) -> None:
+    _check_qubit(sv, q)
     sv.device_state.apply_gate(1, q, 0, theta)
     _touch(sv)
 
 
 def apply_rzz(sv: StateVector, theta: float, qa: int, qb: int) -> None:
+    _check_qubit(sv, qa)
+    _check_qubit(sv, qb)
+    if qa == qb:
+        raise ValidationError("RZZ qubits must differ")
     sv.device_state.apply_gate(2, qa, qb, theta)
     _touch(sv)
 
 
 def apply_gate(sv: StateVector, gate) -> None:
     """One gate, one pass over the state on the GPU (engine.py:158-195)."""
+    for q in gate.qubits:
+        _check_qubit(sv, q)
     q1 = gate.qubits[1] if len(gate.qubits) > 1 else 0
     sv.device_state.apply_gate(_GATE_KIND[gate.kind], gate.qubits[0], q1, gate.theta or 0.0)
     _touch(sv)
+
+
+# scratch device states of the per-gate seam, one per (n, precision)
+_SEAM: dict = {}
+
+
+def _apply_gate_kernel(amps: np.ndarray, gate, qubits: tuple) -> None:
+    """The reference's per-gate seam (engine.py:158-166) on the GPU: the
+    host array is uploaded, the gate runs as one device pass (the same
+    gate kernels as apply_gate), and the result is written back in place.
+    Callers that own device states use apply_gate instead; this keeps code
+    written against the reference's raw-array kernels working."""
+    if amps.dtype not in (np.complex64, np.complex128) or amps.ndim != 1:
+        raise ValidationError("the gate seam works on a flat complex64/complex128 array")
+    n = amps.size.bit_length() - 1
+    if amps.size != 1 << n:
+        raise ValidationError(f"{amps.size} amplitudes do not form a state vector")
+    if gate.kind not in _GATE_KIND:
+        raise ValidationError(f"unknown gate kind {gate.kind!r}")
+    for q in qubits:
+        if not 0 <= q < n:
+            raise ValidationError(f"qubit {q} out of range for {n} qubits")
+    pb = amps.dtype.itemsize
+    dev = _SEAM.get((n, pb))
+    if dev is None:
+        dev = _SEAM[(n, pb)] = _native.DeviceState(n, pb)
+    dev.store_amps(amps)
+    q1 = qubits[1] if len(qubits) > 1 else 0
+    dev.apply_gate(_GATE_KIND[gate.kind], qubits[0], q1, gate.theta or 0.0)
+    amps[...] = dev.copy_amps()
 
 
 def run_circuit(circuit: CircuitIR, precision: Precision | str = Precision.FP32,
@@ -219,7 +305,7 @@ def run_circuit(circuit: CircuitIR, precision: Precision | str = Precision.FP32,
     if cost is not None:
         dev.set_cost(cost)
     dev.run(layers.phase, layers.mixer)
-    return StateVector(circuit.num_qubits, precision, dev, cost)
+    return StateVector._wrap(circuit.num_qubits, precision, dev, cost)
 
 
 # ---------------------------------------------------------------------------
@@ -231,18 +317,17 @@ _EXPECTATION_CHUNK = 1 << 16
 
 def expected_r_from_probs(probs: np.ndarray, inst: WmcInstance) -> float:
     """Expected approximation ratio of an explicit basis-state distribution
-    (engine.py:214-226): chunked probs . C / C*, cut values from the GPU."""
-    from .problem import cut_values_range
-
+    (engine.py:214-226): sum over 2^16 chunks of probs . C_spin / C*, in one
+    device call (lrq_expected_cut); the chunk sums are added in order."""
     probs = np.asarray(probs, dtype=np.float64)
     if probs.size != 1 << inst.num_vertices:
         raise ValidationError(f"distribution over {probs.size} states does not match n={inst.num_vertices}")
     if inst.optimal_cut is None:
         raise StateError("instance has no optimal cut; solve it first")
+    chunks = _native.expected_cut_chunks(inst.num_vertices, inst.weights(), 0.5 * inst.total_weight(), probs)
     total = 0.0
-    for lo in range(0, probs.size, _EXPECTATION_CHUNK):
-        hi = min(lo + _EXPECTATION_CHUNK, probs.size)
-        total += float(probs[lo:hi] @ cut_values_range(inst, lo, hi))
+    for c in chunks:
+        total += float(c)
     return total / inst.optimal_cut.value
 
 
@@ -257,6 +342,43 @@ def exact_expected_r(sv: StateVector, inst: WmcInstance) -> float:
     return float(red.sum_p_cut) / inst.optimal_cut.value
 
 
+@dataclass
+class CutDistribution:
+    """Exact distribution of the cut value C under |psi|^2, binned on the
+    device by the fused final pass (lrq_set_histogram): probs[b] is the total
+    probability of the basis states with C in [edges[b], edges[b+1]).  Plus
+    the pass's extremes: min/max of C over all basis states (C = (W - E)/2)."""
+    edges: np.ndarray
+    probs: np.ndarray
+    cut_min: float
+    cut_max: float
+
+    def bin_of(self, cuts: np.ndarray) -> np.ndarray:
+        b = np.searchsorted(self.edges, np.asarray(cuts, dtype=np.float64), side="right") - 1
+        return np.clip(b, 0, self.probs.size - 1)
+
+
+def exact_cut_distribution(sv, inst: WmcInstance, bins: int = 2048) -> CutDistribution:
+    """The exact C distribution of a state (any engine: dense, sharded,
+    distributed - collective there), from one read-only device pass over the
+    state with the histogram on (chi-square reference of the
+    sampled shots at sizes where |psi|^2 never leaves the device)."""
+    if inst.num_vertices != sv.num_qubits:
+        raise ValidationError(f"instance has {inst.num_vertices} vertices, state has {sv.num_qubits} qubits")
+    if not 1 <= bins <= 4096:
+        raise ValidationError(f"bins must be in [1, 4096], got {bins}")
+    w = inst.weights()
+    W = float(np.sum(np.abs(w)))
+    lo, hi = -W * (1 + 1e-12) - 1e-12, W * (1 + 1e-12) + 1e-12  # E in [-W, W]
+    raw, red = sv._histogram(w, bins, lo, hi)
+    probs = raw.astype(np.float64) / float(1 << 60)
+    e_edges = np.linspace(lo, hi, bins + 1)
+    # C = (W_tot - E) / 2 is decreasing in E: reverse to ascending C
+    wt = inst.total_weight()
+    c_edges = ((wt - e_edges) / 2.0)[::-1]
+    return CutDistribution(c_edges, probs[::-1].copy(), 0.5 * (wt - red.max_energy), 0.5 * (wt - red.min_energy))
+
+
 @dataclass(eq=False)
 class ShotSet:
     num_qubits: int
@@ -269,6 +391,18 @@ class ShotSet:
 
     def bitstrings(self) -> list[str]:
         return [index_to_bitstring(int(z), self.num_qubits) for z in self.indices]
+
+
+def draw_indices(probs: np.ndarray, n_shots: int, rng: np.random.Generator) -> np.ndarray:
+    """Inverse-CDF draw over an unnormalised float64 distribution
+    (engine.py:254-263) on the GPU (lrq_draw_indices): the uniforms come from
+    ``rng`` on the host, the CDF search runs on the device."""
+    if n_shots < 1:
+        raise ValidationError(f"shot count must be positive, got {n_shots}")
+    probs = np.asarray(probs, dtype=np.float64).ravel()
+    if probs.size == 0:
+        raise ValidationError("statevector has zero norm, nothing to sample")
+    return _native.draw_indices(probs, rng.random(n_shots))
 
 
 def sample(sv: StateVector, n_shots: int, rng_seed: int) -> ShotSet:
@@ -317,7 +451,7 @@ def load_statevector(path: str | Path, memory_budget: int | None = None) -> Stat
     chunk = 1 << 24
     for lo in range(0, amps.size, chunk):
         dev.store_amps(amps[lo:lo + chunk], lo)
-    return StateVector(n, precision, dev)
+    return StateVector._wrap(n, precision, dev)
 
 
 def load_statevector_amps(path: str | Path) -> tuple[int, np.ndarray]:

@@ -55,6 +55,7 @@ LAUNCH_KINDS = {
     "N": "search",
     "T": "remap",         # block-transpose exchange of the global qubits
     "Y": "remap (fused)",  # the preceding sweep stored into the peers' buffers; barrier
+    "W": "remap (pipelined)",  # the preceding sweep ran block by block, swaps overlapped; tail wait
     "X": "flip",          # deferred global X: index reversal + mirror exchange
     "S": "small",
     "Z": "finalize",
@@ -295,6 +296,21 @@ class ShardedStateVector:
     def _draw(self, u: np.ndarray) -> np.ndarray:
         return _collective(self._group, self._shards, lambda r, d: d.sample(u))[0]
 
+    def _histogram(self, weights: np.ndarray, bins: int, lo: float, hi: float):
+        w = np.asarray(weights, dtype=np.float64)
+
+        def body(r, d):
+            d.set_cost(w)
+            d.set_histogram(bins, lo, hi)
+            d.recompute()
+            out = (d.histogram(), d.reduce())
+            d.set_histogram(0)
+            return out
+
+        res = _collective(self._group, self._shards, body)
+        self._cost = np.array(w)
+        return res[0]
+
     def norm_squared(self) -> float:
         return float(self._reductions(None).sum_p)
 
@@ -327,7 +343,7 @@ def _rows_from_timings(per_shard: list[tuple[list, str]], nq: int, G: int) -> li
     rows = []
     for i, k in enumerate(kinds):
         ms = max(t[0][i] for t in per_shard) / 1e3
-        if k in "TY":
+        if k in "TYW":
             rows.append(GateTiming(i, k, 0.0, ms, (G - 1) << (nq - g)))
         elif k == "X":
             rows.append(GateTiming(i, k, 0.0, ms, (1 << nq) if G > 1 else 0))
@@ -364,7 +380,7 @@ def run_circuit_sharded(circuit: CircuitIR, plan: ShardPlan, precision: Precisio
         dev.set_timing(False)
         rec = TimingRecord(nq=plan.nq, p=circuit.p, num_shards=G, wall_seconds=time.perf_counter() - wall0,
                            gates=rows)
-        return StateVector(plan.nq, precision, dev, cost), rec
+        return StateVector._wrap(plan.nq, precision, dev, cost), rec
     if devices is None:
         devices = list(range(max(1, _native.device_count())))
     if not devices:

@@ -39,24 +39,21 @@ def _local_energy(nl, m, f, c):
 
 
 def _exchange(state, rank, world, g):
-    """All-to-all block transpose: local block b (top g local bits) <-> rank b's block `rank`."""
+    """All-to-all block transpose (local block b <-> rank b's block `rank`),
+    executed step by step as liblrq's remap schedule says
+    (lrq_describe_remap: XOR-pairwise steps, one partner per step) with gloo
+    send/recv in place of the peer-memory swap / NCCL send-recv."""
     nl = int(np.log2(state.size))
     blocks = state.reshape(world, 1 << (nl - g)).copy()
-    out = blocks.copy()
-    for b in range(world):
-        if b == rank:
-            continue
-        send = torch.from_numpy(blocks[b].view(np.float64).copy())
+    for partner, mine, theirs, half in _native.describe_remap(world, rank):
+        assert theirs == rank and mine == partner and half == (0 if rank < partner else 1)
+        send = torch.from_numpy(blocks[mine].view(np.float64).copy())
         recv = torch.empty_like(send)
-        # lower rank sends first: a fixed order avoids deadlock
-        if rank < b:
-            dist.send(send, b)
-            dist.recv(recv, b)
-        else:
-            dist.recv(recv, b)
-            dist.send(send, b)
-        out[b] = recv.numpy().view(np.complex128)
-    return out.reshape(-1)
+        ops = [dist.P2POp(dist.isend, send, partner), dist.P2POp(dist.irecv, recv, partner)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        blocks[mine] = recv.numpy().view(np.complex128)
+    return blocks.reshape(-1)
 
 
 def _worker(rank, world, port, n, p, seed, q):
@@ -216,3 +213,38 @@ def test_dist_plan_groups_partition_the_local_qubits(g, B):
         last = plan["groups"][-1]
         top = {last["q0"] + i - last["m"] for i in range(last["m"], KA) if (last["tmask"] >> i) & 1}
         assert set(range(nl - g, nl)) <= top
+
+
+@pytest.mark.parametrize("world", [2, 4, 8, 16])
+def test_remap_schedule_is_a_symmetric_xor_pairing(world):
+    """Every off-diagonal block pair (r, b) is swapped exactly once, in the
+    same step on both ranks, and each rank has one partner per step."""
+    seen = {}
+    for r in range(world):
+        steps = _native.describe_remap(world, r)
+        assert len(steps) == world - 1
+        for k, (partner, mine, theirs, half) in enumerate(steps):
+            assert partner == r ^ (k + 1) and mine == partner and theirs == r
+            seen[(r, partner)] = (k, half)
+    for (r, b), (k, half) in seen.items():
+        assert seen[(b, r)][0] == k and seen[(b, r)][1] == 1 - half
+    mirror = _native.describe_remap(world, 1, world - 2)
+    assert mirror == [[world - 2, -1, -1, 0 if 1 < world - 2 else 1]]
+
+
+def test_memory_plan_of_the_headline_configs():
+    """north_star configs 4 and 5 fit one B200 per rank without a spare
+    buffer: n=36 complex128 on 8 GPUs and n=34 complex128 on 2 GPUs hold
+    2^33 amplitudes (128 GiB) per GPU plus < 1 GiB of reductions, cost
+    matrices and staging, inside 170 GB."""
+    for n, world in ((36, 8), (34, 2), (34, 4), (34, 8), (33, 1)):
+        m = _native.describe_memory(n, 16, world, 3)
+        g = world.bit_length() - 1
+        assert m["state"] == 16 << (n - g)
+        assert m["other"] < (1 << 30)
+        assert m["state"] + m["other"] <= 170e9, (n, world, m)
+    # the fused remap's spare buffer only fits at half the state
+    m = _native.describe_memory(34, 16, 8, 3)
+    assert m["state"] + m["spare"] + m["other"] < 170e9
+    m = _native.describe_memory(36, 16, 8, 3)
+    assert m["state"] + m["spare"] > 183e9

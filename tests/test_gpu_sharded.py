@@ -149,21 +149,69 @@ def test_larger_sharded_runs_match_dense(n, G, p, prec, dbeta):
         sv.release()
 
 
-@pytest.mark.parametrize("n,G,p,prec", [(16, 2, 3, "fp64"), (18, 4, 2, "fp32"), (26, 8, 3, "fp64")])
-def test_fused_remap_equals_swap_remap(monkeypatch, n, G, p, prec):
-    """The fused remap (the group-A sweep stores each block into its owner's
-    next buffer) moves exactly what the separate block swap moves: the
-    amplitudes are bitwise identical."""
+REMAP_MODES = {"fused": ("1", "1", "Y"), "pipelined": ("0", "1", "W"), "serial": ("0", "0", "T")}
+
+
+@pytest.mark.parametrize("n,G,p,prec", [(16, 2, 3, "fp64"), (18, 4, 2, "fp32"), (26, 8, 3, "fp64"),
+                                        (27, 8, 4, "fp32"), (25, 2, 3, "fp64")])
+def test_remap_transports_are_bitwise_equal(monkeypatch, n, G, p, prec):
+    """The three remap forms move exactly the same amplitudes, so the states
+    are bitwise identical: fused (the group-A sweep stores each block into
+    its owner's spare buffer), pipelined (the group-A sweep runs block by
+    block in XOR order and each finished block is swapped in place with its
+    owner on a second stream while the next block is swept: the form used
+    when no spare buffer fits) and serial (sweep, then the XOR swaps)."""
     circ = L.build_circuit(L.generate_instance(n, 6), L.LrQaoaParams(p=p, delta_beta=0.9))
     out = {}
-    for flag in ("1", "0"):
-        monkeypatch.setenv("LRQ_FUSED_REMAP", flag)
+    for mode, (fused, pipe, tag) in REMAP_MODES.items():
+        monkeypatch.setenv("LRQ_FUSED_REMAP", fused)
+        monkeypatch.setenv("LRQ_PIPELINED_REMAP", pipe)
         sv, rec = L.run_circuit_sharded(circ, L.plan_for_shard_count(n, G), prec)
-        out[flag] = (sv.amps.copy(), None, [g.kind for g in rec.gates])
+        kinds = [g.kind for g in rec.gates]
+        out[mode] = (sv.amps.copy(), kinds, L.sample(sv, 500, rng_seed=2).indices)
+        assert tag in kinds, (mode, kinds)
         sv.release()
-    np.testing.assert_array_equal(out["1"][0], out["0"][0])
-    assert "Y" in out["1"][2] and "Y" not in out["0"][2]
-    assert [k.replace("Y", "T") for k in out["1"][2]] == out["0"][2]
+    for mode in ("pipelined", "serial"):
+        np.testing.assert_array_equal(out[mode][0], out["fused"][0])
+        np.testing.assert_array_equal(out[mode][2], out["fused"][2])
+    # the same sweeps; only the remap records differ (the odd-p restoring
+    # remap follows a high-group sweep and is never fused or pipelined)
+    strip = lambda ks: [k for k in ks if k not in "YWT"]  # noqa: E731
+    assert strip(out["fused"][1]) == strip(out["pipelined"][1]) == strip(out["serial"][1])
+
+
+def test_shards_at_the_hbm_limit_take_the_pipelined_remap():
+    """n=33 complex128 over 8 shards on ONE B200: 8 x 16 GiB = 128 GiB, so
+    the fused remap's spare buffers (another 128 GiB) do not fit and the
+    group takes the in-place pipelined remap.  Checked against the dense
+    complex128 run of the same circuit (run first, then freed): exact r,
+    norm, the max-cut argmax, sampled shots and amplitude ranges."""
+    n, G, p = 33, 8, 3
+    inst = L.generate_instance(n, 1)
+    circ = L.build_circuit(inst, L.LrQaoaParams(p=p))
+    budget = 1 << 40
+    dense = L.run_circuit(circ, "fp64", memory_budget=budget)
+    red_d = dense.device_state.reduce()
+    rng = np.random.default_rng(0)
+    starts = [int(x) for x in rng.integers(0, (1 << n) - (1 << 20), size=4)] + [(1 << n) - (1 << 20)]
+    ranges_d = [dense._copy_range(s0, 1 << 20) for s0 in starts]
+    shots_d = L.sample(dense, 2000, rng_seed=5).indices
+    dense.release()
+    _native.drain_pool()
+    sv, rec = L.run_circuit_sharded(circ, L.plan_for_shard_count(n, G), "fp64", memory_budget=budget)
+    try:
+        kinds = [g.kind for g in rec.gates]
+        assert "W" in kinds and "Y" not in kinds, kinds
+        red = sv._reductions(None)
+        assert red.sum_p == pytest.approx(red_d.sum_p, rel=1e-12)
+        assert red.sum_p_cut == pytest.approx(red_d.sum_p_cut, rel=1e-11)
+        assert int(red.argmax_cut) == int(red_d.argmax_cut)
+        for s0, want in zip(starts, ranges_d):
+            assert normwise(sv._copy_range(s0, 1 << 20), want) < 1e-12
+        shots = L.sample(sv, 2000, rng_seed=5).indices
+        assert int(np.sum(shots != shots_d)) <= 4
+    finally:
+        sv.release()
 
 
 def test_distributed_api_with_one_rank_runs_the_single_gpu_engine():
