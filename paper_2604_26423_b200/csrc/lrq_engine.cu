@@ -211,6 +211,7 @@ struct lrq_state {
   int hist_bins = 0;
   double hist_lo = 0.0, hist_hi = 0.0;
   bool hist_summed = false;  // NCCL ranks: dhist already holds the sum over ranks
+  bool hist_valid = false;   // a reducing pass has filled dhist since lrq_set_histogram
 };
 
 namespace {
@@ -569,7 +570,7 @@ int launch_small(const SmallParams& sp, size_t smem, cudaStream_t st, int grid =
 }
 
 int launch_small_any(int pbytes, const SmallParams& sp, cudaStream_t st) {
-  const size_t smem = (size_t)pbytes * (1u << sp.n) + 8 * 4 * 8;
+  const size_t smem = (size_t)pbytes * (1u << sp.n) + 8 * 5 * 8;
   return pbytes == 8 ? launch_small<float>(sp, smem, st) : launch_small<double>(sp, smem, st);
 }
 
@@ -589,6 +590,7 @@ void record(lrq_state* s, size_t idx, char kind) {
 template <typename PR>
 void set_hist(lrq_state* s, PR& sp) {
   if (!s->dhist) return;
+  s->hist_valid = true;  // filled by the pass being set up
   sp.hist = s->dhist;
   sp.hist_bins = s->hist_bins;
   sp.hist_lo = s->hist_lo;
@@ -2003,7 +2005,7 @@ int lrq_noisy_batch(int n, int pbytes, int device, int trajectories, int p, cons
     sp.probs = dprobs;
     sp.init_re = pbytes == 8 ? init_amplitude<float>(n) : init_amplitude<double>(n);
     sp.min_bit = -2;
-    const size_t smem = (size_t)pbytes * N + 8 * 4 * 8;
+    const size_t smem = (size_t)pbytes * N + 8 * 5 * 8;
     if (pbytes == 8) {
       rc = launch_small<float>(sp, smem, st, trajectories);
     } else {
@@ -2530,14 +2532,14 @@ int lrq_set_histogram(lrq_state* s, int bins, double lo, double hi) {
   s->hist_bins = bins;
   s->hist_lo = lo;
   s->hist_hi = hi;
-  s->reduced = false;  // the next reducing pass fills it
+  s->hist_valid = false;  // the next reducing pass fills it (the other reductions stay valid)
   return LRQ_OK;
 }
 
 int lrq_get_histogram(lrq_state* s, uint64_t* raw) {
   if (!s || !raw) return fail(LRQ_EVALIDATION, "null argument");
   if (!s->dhist) return fail(LRQ_ERUNTIME, "no histogram: call lrq_set_histogram, then run or recompute");
-  if (!s->reduced) return fail(LRQ_ERUNTIME, "no reductions: run the circuit or recompute first");
+  if (!s->hist_valid) return fail(LRQ_ERUNTIME, "no histogram yet: run the circuit or recompute after lrq_set_histogram");
   DeviceGuard guard(s->device);
   const int B = s->hist_bins;
   if (s->world > 1 && !s->group) {
