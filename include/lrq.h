@@ -105,6 +105,13 @@ int lrq_noisy_batch(int num_qubits, int precision_bytes, int device, int traject
                     const double *mixer, const unsigned *xmask, int64_t shots, const double *u, double *probs_out,
                     uint64_t *idx_out);
 
+/* Whether the fused final pass (and lrq_recompute) also searches min E with
+ * its lowest-index argmin (the exhaustive max cut, problem.py:174-211) and
+ * max E.  On by default; a caller that already knows C* turns it off and the
+ * pass only sums p and p*E (min_energy / max_energy / argmax_cut then read
+ * +inf / -inf / ~0).                                                       */
+int lrq_set_search(lrq_state *s, int on);
+
 /* reductions of the last run (exact_expected_r numerator, engine.py:214-226;
  * exhaustive max cut argmax, problem.py:174-211).                            */
 int lrq_reduce(lrq_state *s, lrq_reduction *out);

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "lrq_draw_indices": ([_p, _c_u64, _p, _c_i64, _p, _c_int], _c_int),
     "lrq_set_timing": ([_state_p, _c_int], _c_int),
     "lrq_set_histogram": ([_state_p, _c_int, _c_dbl, _c_dbl], _c_int),
+    "lrq_set_search": ([_state_p, _c_int], _c_int),
     "lrq_get_histogram": ([_state_p, _p], _c_int),
     "lrq_get_timings": ([_state_p, _p, ctypes.c_char_p, _c_int, ctypes.POINTER(_c_int)], _c_int),
     "lrq_stream": ([_state_p, ctypes.POINTER(_p)], _c_int),
@@ -217,6 +218,7 @@ class DeviceState:
         if h is not None:
             self._h = h
             self.set_cost(np.zeros(n * (n - 1) // 2))
+            self.set_search(True)
             return
         h = _state_p()
         try:
@@ -368,6 +370,10 @@ class DeviceState:
         dt = np.complex64 if self.precision_bytes == 8 else np.complex128
         amps = np.ascontiguousarray(amps, dtype=dt)
         check(lib().lrq_store_amps(self.handle, int(start), int(amps.size), ptr(amps)))
+
+    def set_search(self, on: bool) -> None:
+        """Whether reducing passes search the max cut (min E, argmin, max E)."""
+        check(lib().lrq_set_search(self.handle, 1 if on else 0))
 
     def set_histogram(self, bins: int, lo: float = 0.0, hi: float = 1.0) -> None:
         """p-weighted E histogram of the next reducing pass (bins = 0: off)."""

@@ -34,6 +34,7 @@ struct SmallParams {
   double* red_minE;
   unsigned long long* red_arg;
   double* red_maxE;              // may be null
+  int search;                    // unused here: the whole-state path always searches (tiny n)
   unsigned long long* hist;      // global energy histogram (may be null), see SweepParams
   int hist_bins;
   double hist_lo, hist_scale;

@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing without a profiler attached
+
 #include "../../include/lrq.h"
 #include "lrq_aux.cuh"
 #include "lrq_plan.h"
@@ -52,6 +54,21 @@ constexpr int kFinScratch = 6 * kFinBlocks;
 // amplitudes (pair = 1 for complex64: a unit holds two amplitudes)
 inline int pair_of(int pbytes) { return pbytes == 8 ? 1 : 0; }
 inline int tile_amp_bits(int pbytes) { return kUnitBits + pair_of(pbytes); }
+
+// NVTX range over a host scope (nsys / ncu --nvtx show the engine's phases:
+// runs, sweeps by kind and group, remaps, sampling)
+struct NvtxRange {
+  explicit NvtxRange(const char* msg) { nvtxRangePushA(msg); }
+  NvtxRange(const char* a, const char* b) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "%s%s", a, b);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+const char* group_name(int gk) { return gk == GK_A ? "(A)" : gk == GK_H4 ? "(H4)" : "(H)"; }
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -212,6 +229,7 @@ struct lrq_state {
   double hist_lo = 0.0, hist_hi = 0.0;
   bool hist_summed = false;  // NCCL ranks: dhist already holds the sum over ranks
   bool hist_valid = false;   // a reducing pass has filled dhist since lrq_set_histogram
+  bool search = true;        // reducing passes search min E / argmin / max E (lrq_set_search)
 };
 
 namespace {
@@ -589,6 +607,7 @@ void record(lrq_state* s, size_t idx, char kind) {
 // the engine stream before the pass, filled by the pass's integer atomics
 template <typename PR>
 void set_hist(lrq_state* s, PR& sp) {
+  sp.search = s->search ? 1 : 0;
   if (!s->dhist) return;
   s->hist_valid = true;  // filled by the pass being set up
   sp.hist = s->dhist;
@@ -1074,6 +1093,8 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
       sp.rbits = tb - g;
       for (int b = 0; b < s->world; ++b) sp.rdst[b] = (char*)s->peer[next][b] + (size_t)s->rank * blockBytes;
     }
+    const char kname[2] = {"PMFRLQN"[w.kind], 0};
+    NvtxRange nv_sweep("sweep ", kname);
     // pipelined remap: the group-A sweep runs block by block in XOR order
     // (block rank ^ j at step j) and each finished block is swapped with its
     // owner while the next block is swept (remap_exchange on the remap stream)
@@ -1110,10 +1131,12 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
       s->amps = s->bufs[s->cur];
       record(s, ev++, 'Y');
     } else if (pipe) {
+      NvtxRange nv_remap("remap pipelined");
       rc = remap_exchange(s, true, -1);
       if (rc) return rc;
       record(s, ev++, 'W');
     } else if (w.remap_after) {
+      NvtxRange nv_remap("remap serial");
       rc = remap_exchange(s, false, -1);
       if (rc) return rc;
       record(s, ev++, 'T');
@@ -1638,6 +1661,7 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
   for (int k = 0; k < p; ++k)
     if (!isfinite(mixer[k])) return fail(LRQ_EVALIDATION, "mixer angle is not finite");
   DeviceGuard guard(s->device);
+  NvtxRange nv_run(s->world > 1 ? "lrq_run (distributed)" : "lrq_run");
   if (s->world > 1) {
     const int rc = run_dist(s, p, phase, mixer);
     if (rc && s->group) group_abort(s->group, g_err);
@@ -1789,6 +1813,8 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
         if (const int rh = zero_hist(s)) return rh;
         set_hist(s, sp);
       }
+      char kname[2] = {"PMFRLQN"[w.kind], 0};
+      NvtxRange nv_sweep(kname, group_name(g.kind));
       int rc = w.prog == 1 ? launch_wd(s, g.kind, w.kind, sp) : launch_sweep(s, g.kind, w.kind, sp, grid);
       if (rc) return rc;
       record(s, ev++, "PMFRLQN"[w.kind]);
@@ -2036,6 +2062,7 @@ int lrq_noisy_batch(int n, int pbytes, int device, int trajectories, int p, cons
 
 int lrq_recompute(lrq_state* s) {
   if (!s) return fail(LRQ_EVALIDATION, "null state");
+  NvtxRange nv("lrq_recompute");
   if (!s->ran) return fail(LRQ_ERUNTIME, "state holds no circuit result yet");
   DeviceGuard guard(s->device);
   const int n = s->n;
@@ -2158,6 +2185,7 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   if (shots < 1) return fail(LRQ_EVALIDATION, "shot count must be positive, got " + std::to_string(shots));
   if (!s->reduced) return fail(LRQ_ERUNTIME, "no CDF: set a cost and run the circuit first");
   DeviceGuard guard(s->device);
+  NvtxRange nv("lrq_sample");
   double total = 0.0, off = 0.0;
   unsigned long long base_index = 0;
   if (s->world > 1) {
@@ -2512,6 +2540,12 @@ int lrq_max_cut(int n, const double* w, int device, uint64_t* argmax, double* va
   }
   *argmax = best;
   return lrq_cut_values(n, w, &best, 0, 1, value, device);
+}
+
+int lrq_set_search(lrq_state* s, int on) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  s->search = on != 0;
+  return LRQ_OK;
 }
 
 int lrq_set_histogram(lrq_state* s, int bins, double lo, double hi) {

@@ -144,6 +144,7 @@ struct SweepParams {
   double* red_minE;
   unsigned long long* red_arg;
   double* red_maxE;  // per-tile max E (may be null)
+  int search;        // reductions: 1 = also min E with argmin (max-cut search) and max E
   // p-weighted energy histogram (may be null): bin b = floor((E - hist_lo) *
   // hist_scale) clamped to [0, hist_bins); each amplitude adds round(p 2^60)
   // to its bin as a 64-bit integer, so the totals do not depend on the order

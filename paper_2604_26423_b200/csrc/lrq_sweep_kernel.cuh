@@ -120,6 +120,30 @@ struct SweepTile {
     }
   }
 
+  template <bool SEARCH, bool HIST>
+  __device__ static __forceinline__ void reduce_loop(Ctx& c, const SweepParams& P, const double (&Elo)[4],
+                                                     const double (&Ehi)[NV / 4], unsigned vmask, bool thread_ok,
+                                                     double& sp_, double& spe, double& mine, double& maxe,
+                                                     int& bestv) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double ev = (Elo[v & 3] + Ehi[v >> 2]) + c.ERR[v];
+      if constexpr (AMPS) {
+        const double pv = prob(amp_get(c.r, v));
+        sp_ += pv;
+        spe = fma(pv, ev, spe);
+        if constexpr (HIST) hist_add(c.shist, P.hist_bins, P.hist_lo, P.hist_scale, ev, pv);
+      }
+      if constexpr (SEARCH) {
+        maxe = fmax(maxe, ev);
+        if (thread_ok && !(v & vmask) && ev < mine) {
+          mine = ev;
+          bestv = v;
+        }
+      }
+    }
+  }
+
   __device__ static __forceinline__ void reduce(Ctx& c, int lo) {
     const SweepParams& P = *c.P;
     const double* th = c.thrW;
@@ -154,21 +178,18 @@ struct SweepTile {
     double sp_ = 0.0, spe = 0.0, mine = __longlong_as_double(0x7ff0000000000000ll);
     double maxe = -__longlong_as_double(0x7ff0000000000000ll);
     int bestv = NV;
-    unsigned long long* shist = c.shist;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double ev = (Elo[v & 3] + Ehi[v >> 2]) + c.ERR[v];
-      if constexpr (AMPS) {
-        const double pv = prob(amp_get(c.r, v));
-        sp_ += pv;
-        spe = fma(pv, ev, spe);
-        if (shist) hist_add(shist, P.hist_bins, P.hist_lo, P.hist_scale, ev, pv);
-      }
-      maxe = fmax(maxe, ev);
-      if (thread_ok && !(v & vmask) && ev < mine) {
-        mine = ev;
-        bestv = v;
-      }
+    // the per-amplitude loop in three compile-time forms: plain sums (the
+    // max-cut optimum already known), + min/argmin/max E search, + histogram
+    if (!AMPS || P.search) {
+      if (AMPS && c.shist)
+        reduce_loop<true, true>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+      else
+        reduce_loop<true, false>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+    } else {
+      if (c.shist)
+        reduce_loop<false, true>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+      else
+        reduce_loop<false, false>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
     }
     unsigned long long zbest = ~0ull;
     if (bestv < NV) {

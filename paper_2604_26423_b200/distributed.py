@@ -119,6 +119,21 @@ class DistStateVector:
         dt = np.complex128 if self._precision is Precision.FP64 else np.complex64
         return np.concatenate([p.numpy().view(dt) for p in parts])
 
+    def save(self, path) -> None:
+        """Collective LQSV dump (engine.py:279-293 format): rank 0 writes the
+        header and sizes the file, then every rank streams its own shard into
+        its byte range (ranks share the node's filesystem)."""
+        import torch.distributed as dist
+
+        from .engine import lqsv_create, lqsv_write_range
+
+        if self.rank == 0:
+            lqsv_create(path, self.num_qubits, self._precision)
+        dist.barrier(group=self._group)
+        L = 1 << self.n_local
+        lqsv_write_range(path, self._dev, self.rank * L, L, self._precision)
+        dist.barrier(group=self._group)
+
     def release(self) -> None:
         """Park the shard for the next run_circuit_distributed of the same
         shape (all ranks release in step, so the pools stay symmetric)."""
@@ -168,6 +183,32 @@ def enable_fused_remap(dev: _native.DeviceState, group=None) -> bool:
     return enable_peer_remap(dev, group) == "fused"
 
 
+def load_statevector_distributed(path, group=None, device: int | None = None) -> DistStateVector:
+    """Collective: every rank reads its own shard of an LQSV dump straight
+    into its device (no host holds the whole state)."""
+    import torch.distributed as dist
+
+    from .engine import lqsv_header, lqsv_read_range
+
+    n, precision, _ = lqsv_header(path)
+    rank, world = _world(group)
+    if world & (world - 1):
+        raise ValidationError(f"world size must be a power of two, got {world}")
+    dev_index = _native.default_device() if device is None else int(device)
+    if world == 1:
+        dev = _native.DeviceState(n, precision.bytes_per_amplitude, dev_index)
+    else:
+        box = [_native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        dev = _native.DeviceState.create_dist(n, precision.bytes_per_amplitude, dev_index, rank, world, box[0])
+        dev.remap_mode = enable_peer_remap(dev, group)
+    L = 1 << (n - (world.bit_length() - 1))
+    lqsv_read_range(path, dev, rank * L, L, precision)
+    dev.set_cost(np.zeros(n * (n - 1) // 2))
+    dev.recompute()
+    return DistStateVector(n, precision, dev, rank, world, group, None)
+
+
 def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Precision.FP32, group=None,
                             device: int | None = None, memory_budget: int | None = None) -> DistStateVector:
     """Collective run of an LR-QAOA circuit over all ranks of `group`."""
@@ -194,5 +235,6 @@ def run_circuit_distributed(circuit: CircuitIR, precision: Precision | str = Pre
         dev.remap_mode = enable_peer_remap(dev, group)
     cost = getattr(circuit, "cost_weights", None)
     dev.set_cost(cost if cost is not None else np.zeros(n * (n - 1) // 2))
+    dev.set_search(getattr(circuit, "cost_optimum", None) is None)  # C* known: no max-cut search
     dev.run(layers.phase, layers.mixer)
     return DistStateVector(n, precision, dev, rank, world, group, cost)

@@ -176,6 +176,7 @@ class StateVector:
         """One read-only pass with the E histogram on: (raw bins, reductions)."""
         dev = self.device_state
         dev.set_cost(weights)
+        dev.set_search(True)  # the extremes of C come from the same pass
         dev.set_histogram(bins, lo, hi)
         try:
             dev.recompute()
@@ -304,6 +305,8 @@ def run_circuit(circuit: CircuitIR, precision: Precision | str = Precision.FP32,
     cost = getattr(circuit, "cost_weights", None)
     if cost is not None:
         dev.set_cost(cost)
+    # a solved instance's C* is known: the final pass only sums p and p*C
+    dev.set_search(getattr(circuit, "cost_optimum", None) is None)
     dev.run(layers.phase, layers.mixer)
     return StateVector._wrap(circuit.num_qubits, precision, dev, cost)
 
@@ -420,37 +423,81 @@ _MAGIC = b"LQSV"
 _HEADER = struct.Struct("<4sBBH")
 
 
-def save_statevector(sv: StateVector, path: str | Path) -> None:
-    fbytes = sv.precision.bytes_per_amplitude // 2
-    code = "<c8" if sv.precision is Precision.FP32 else "<c16"
-    with open(path, "wb") as fh:
-        fh.write(_HEADER.pack(_MAGIC, 1, fbytes, sv.num_qubits))
-        chunk = 1 << 24
-        total = 1 << sv.num_qubits
-        for lo in range(0, total, chunk):
-            part = sv._copy_range(lo, min(chunk, total - lo))
-            fh.write(np.ascontiguousarray(part, dtype=code).tobytes())
+_DUMP_CHUNK = 1 << 24  # amplitudes per host round trip of a streamed dump / load
 
 
-def load_statevector(path: str | Path, memory_budget: int | None = None) -> StateVector:
-    """LQSV dump -> a state in HBM (engine.py:296-312), streamed in chunks."""
-    raw = Path(path).read_bytes()
-    if len(raw) < _HEADER.size:
+def lqsv_header(path: str | Path) -> tuple[int, "Precision", int]:
+    """(num_qubits, precision, payload offset) of an LQSV dump, validated
+    like the reference's loader (engine.py:296-312) without reading the payload."""
+    p = Path(path)
+    size = p.stat().st_size if p.exists() else 0
+    with open(p, "rb") as fh:
+        head = fh.read(_HEADER.size)
+    if len(head) < _HEADER.size:
         raise ValidationError(f"{path} is not a statevector dump (truncated header)")
-    magic, version, fbytes, n = _HEADER.unpack_from(raw)
+    magic, version, fbytes, n = _HEADER.unpack_from(head)
     if magic != _MAGIC or version != 1:
         raise ValidationError(f"{path} is not a statevector dump (bad magic/version)")
     if fbytes not in (4, 8):
         raise ValidationError(f"{path} has unsupported float width {fbytes}")
     precision = Precision.FP32 if fbytes == 4 else Precision.FP64
-    code = "<c8" if fbytes == 4 else "<c16"
-    amps = np.frombuffer(raw, dtype=code, offset=_HEADER.size)
-    if amps.size != 1 << n:
-        raise ValidationError(f"{path} payload has {amps.size} amplitudes, expected {1 << n}")
+    want = _HEADER.size + (precision.bytes_per_amplitude << n)
+    if size != want:
+        amps = (size - _HEADER.size) // precision.bytes_per_amplitude
+        raise ValidationError(f"{path} payload has {amps} amplitudes, expected {1 << n}")
+    return n, precision, _HEADER.size
+
+
+def lqsv_create(path: str | Path, num_qubits: int, precision: "Precision") -> None:
+    """Write the header and size the file: ranks / shards then fill their
+    own byte ranges (lqsv_write_range) in any order, concurrently."""
+    fbytes = precision.bytes_per_amplitude // 2
+    with open(path, "wb") as fh:
+        fh.write(_HEADER.pack(_MAGIC, 1, fbytes, num_qubits))
+        fh.truncate(_HEADER.size + (precision.bytes_per_amplitude << num_qubits))
+
+
+def lqsv_write_range(path: str | Path, dev, global_start: int, count: int, precision: "Precision") -> None:
+    """Stream the local amplitudes [0, count) of device state `dev` into the
+    dump at global index global_start (little-endian re/im, chunked D2H)."""
+    code = "<c8" if precision is Precision.FP32 else "<c16"
+    B = precision.bytes_per_amplitude
+    with open(path, "r+b") as fh:
+        fh.seek(_HEADER.size + global_start * B)
+        for lo in range(0, count, _DUMP_CHUNK):
+            part = dev.copy_amps(lo, min(_DUMP_CHUNK, count - lo))
+            fh.write(np.ascontiguousarray(part, dtype=code).tobytes())
+
+
+def lqsv_read_range(path: str | Path, dev, global_start: int, count: int, precision: "Precision") -> None:
+    """Stream the dump's amplitudes [global_start, +count) into the local
+    amplitudes [0, count) of device state `dev` (chunked H2D)."""
+    code = "<c8" if precision is Precision.FP32 else "<c16"
+    B = precision.bytes_per_amplitude
+    with open(path, "rb") as fh:
+        fh.seek(_HEADER.size + global_start * B)
+        for lo in range(0, count, _DUMP_CHUNK):
+            m = min(_DUMP_CHUNK, count - lo)
+            dev.store_amps(np.frombuffer(fh.read(m * B), dtype=code), lo)
+
+
+def save_statevector(sv, path: str | Path) -> None:
+    """LQSV dump (engine.py:279-293 format) streamed from the device in
+    chunks; a sharded state writes every shard's range from its own thread
+    (sharded.ShardedStateVector.save), a distributed one from every rank
+    (distributed.DistStateVector.save)."""
+    if hasattr(sv, "save"):
+        sv.save(path)
+        return
+    lqsv_create(path, sv.num_qubits, sv.precision)
+    lqsv_write_range(path, sv.device_state, 0, 1 << sv.num_qubits, sv.precision)
+
+
+def load_statevector(path: str | Path, memory_budget: int | None = None) -> StateVector:
+    """LQSV dump -> a state in HBM (engine.py:296-312), streamed in chunks."""
+    n, precision, _ = lqsv_header(path)
     dev = _device_state(n, precision, memory_budget)
-    chunk = 1 << 24
-    for lo in range(0, amps.size, chunk):
-        dev.store_amps(amps[lo:lo + chunk], lo)
+    lqsv_read_range(path, dev, 0, 1 << n, precision)
     return StateVector._wrap(n, precision, dev)
 
 

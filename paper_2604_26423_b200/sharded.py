@@ -322,6 +322,15 @@ class ShardedStateVector:
         a = self.amps.astype(np.complex128, copy=False)
         return (a.real ** 2 + a.imag ** 2).astype(np.float64)
 
+    def save(self, path) -> None:
+        """LQSV dump written by every shard's thread into its own byte range."""
+        from .engine import lqsv_create, lqsv_write_range
+
+        lqsv_create(path, self.num_qubits, self._precision)
+        L = 1 << self._shards[0].n_local
+        _collective(self._group, self._shards,
+                    lambda r, d: lqsv_write_range(path, d, r * L, L, self._precision))
+
     def release(self) -> None:
         for s in self._shards:
             s.close(park=False)
@@ -408,6 +417,40 @@ def run_circuit_sharded(circuit: CircuitIR, plan: ShardPlan, precision: Precisio
     return ShardedStateVector(plan, precision, group, shards, cost), rec
 
 
+def load_statevector_sharded(path, plan: ShardPlan, devices: list[int] | None = None) -> ShardedStateVector:
+    """An LQSV dump loaded into plan.num_shards shard states (one host thread
+    per shard reads its own byte range), e.g. a dump larger than one device."""
+    from .engine import lqsv_header, lqsv_read_range
+
+    n, precision, _ = lqsv_header(path)
+    if n != plan.nq:
+        raise ValidationError(f"dump has {n} qubits but the plan covers {plan.nq}")
+    G = plan.num_shards
+    if devices is None:
+        devices = list(range(max(1, _native.device_count())))
+    group = _native.ShardGroup(G)
+    shards = []
+    try:
+        for s in range(G):
+            shards.append(_native.DeviceState.create_shard(n, precision.bytes_per_amplitude,
+                                                           devices[s * len(devices) // G], s, group))
+        L = 1 << shards[0].n_local
+        zero = np.zeros(n * (n - 1) // 2)
+
+        def body(r, d):
+            lqsv_read_range(path, d, r * L, L, precision)
+            d.set_cost(zero)
+            d.recompute()
+
+        _collective(group, shards, body)
+    except BaseException:
+        for d in shards:
+            d.close(park=False)
+        group.close()
+        raise
+    return ShardedStateVector(plan, precision, group, shards, None)
+
+
 # ---------------------------------------------------------------------------
 # scaling sweeps (sharded.py:388-450)
 
@@ -465,4 +508,5 @@ __all__ = [
     "ExchangeStep", "GateTiming", "LAUNCH_KINDS", "ShardPlan", "ShardedStateVector", "SweepConfig",
     "TIMING_CSV_FIELDS", "TimingRecord", "exchange_steps", "exchange_volume", "plan_for_shard_count",
     "plan_shards", "remap_volume", "run_circuit_sharded", "scaling_sweep", "write_timing_csv",
+    "load_statevector_sharded",
 ]

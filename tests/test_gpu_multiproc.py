@@ -67,6 +67,13 @@ def _worker(rank, world, port, n, p, prec, env, out_path, fail_rank):
             amps = sv.gather_amps()
             if rank == 0:
                 result["amps"] = amps
+            # per-rank streamed LQSV dump and load
+            path = out_path + ".lqsv"
+            sv.save(path)
+            from paper_2604_26423_b200.distributed import load_statevector_distributed
+            back = load_statevector_distributed(path)
+            result["reload_equal"] = bool(np.array_equal(back.local_amps(), sv.local_amps()))
+            back.release()
         except L.AbortedRunError as exc:
             result["aborted"] = str(exc)
         sv.release()
@@ -116,6 +123,10 @@ def test_nccl_ranks_match_the_dense_engine(world, transport, tmp_path):
     other = L.solve_instance(L.generate_instance(n, 9), limit=n)
     assert res["r_other"] == pytest.approx(L.exact_expected_r(dense, other), rel=1e-12)
     assert int(np.sum(res["shots"] != L.sample(dense, 3000, rng_seed=1).indices)) <= 2
+    assert res["reload_equal"]
+    from paper_2604_26423_b200.engine import load_statevector_amps
+    n_file, amps = load_statevector_amps(out + ".lqsv")
+    assert n_file == n and amps.tobytes() == res["amps"].astype(np.complex128).tobytes()
     dense.release()
 
 
