@@ -23,6 +23,7 @@
 #include "lrq_dist.cuh"
 #include "lrq_sweep_tma.cuh"
 #include "lrq_sweep_wd.cuh"
+#include "lrq_sweep_wdc.cuh"
 
 using namespace lrq;
 
@@ -68,7 +69,9 @@ struct NvtxRange {
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
-const char* group_name(int gk) { return gk == GK_A ? "(A)" : gk == GK_H4 ? "(H4)" : "(H)"; }
+const char* group_name(int gk) {
+  return gk == GK_A ? "(A)" : gk == GK_H4 ? "(H4)" : gk == GK_C10 ? "(C10)" : gk == GK_C9 ? "(C9)" : gk == GK_C8 ? "(C8)" : "(H)";
+}
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -389,6 +392,16 @@ bool make_tile_tmap(CUtensorMap* tm, void* amps, int gk, int n, int pbytes, int 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   const int nrb = KA - MA;
+  if (pbytes == 8 && MA >= 5) {
+    // cluster groups with runs longer than the 128 B swizzle span: each run is
+    // 2^(MA-4) rows of 16 elements (like the complex128 H tile), natural order
+    cuuint64_t dims[5] = {16, 1ull << (MA - 4), 1ull << (q0 - MA), 1ull << nrb, 1ull << (n - q0 - nrb)};
+    cuuint64_t strides[4] = {128, (1ull << MA) * B, (1ull << q0) * B, (1ull << (q0 + nrb)) * B};
+    cuuint32_t box[5] = {16, (cuuint32_t)(1u << (MA - 4)), 1, (cuuint32_t)(1u << nrb), 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   if (pbytes == 8) {
     // 64 B runs (MA = 3) use the 64B swizzle: a swizzled box row is padded
     // to the swizzle width, so 64 B rows under the 128B mode would not fit
@@ -515,6 +528,63 @@ int launch_wd(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
   }
   if (gk == GK_H) return launch_wd_kind<float, GK_H>(s->stream, sk, sp, g, smem);
   return launch_wd_kind<float, GK_H4>(s->stream, sk, sp, g, smem);
+}
+
+template <int GK, int SK, int TEAMS>
+int launch_wdc_t(cudaStream_t st, const SweepParams& sp, int grid, size_t smem) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(sweep_wdc_kernel<GK, SK, TEAMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024);
+  });
+  CUDA_TRY(err);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(TEAMS * kWdWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;  // the CTA pair sharing one 128 KB tile
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, sweep_wdc_kernel<GK, SK, TEAMS>, sp));
+  return LRQ_OK;
+}
+
+template <int GK>
+int launch_wdc_kind(cudaStream_t st, int sk, const SweepParams& sp, int grid, size_t smem) {
+  if (sk == SK_F) return launch_wdc_t<GK, SK_F, 2>(st, sp, grid, smem);
+  if (sk == SK_P) return launch_wdc_t<GK, SK_P, 2>(st, sp, grid, smem);  // 2 teams: 255 registers, no spills
+  return launch_wdc_t<GK, SK_M, 2>(st, sp, grid, smem);
+}
+
+// cluster-pair sweep of a complex64 C group (plan prog 2): 148 CTAs = 74
+// pairs, each pair one 128 KB tile at a time, three 64 KB stages per CTA
+int launch_wdc(lrq_state* s, int gk, int sk, const SweepParams& sp_in) {
+  SweepParams sp = sp_in;
+  const int K = tile_amp_bits(s->pbytes);
+  const int ma = group_ma(gk, pair_of(s->pbytes));
+  if (s->pbytes != 8) return fail(LRQ_ERUNTIME, "internal: cluster groups are complex64");
+  if (!make_tile_tmap(&sp.tmap, sp.amps, gk, sp.n, s->pbytes, ma, K, sp.q0, sp.num_tiles))
+    return fail(LRQ_ERUNTIME, "cuTensorMapEncodeTiled failed for the cluster sweep tile map");
+  sp.has_tmap = 1;
+  sp.nstages = 3;
+  const size_t smem = wdc_smem_bytes(sp.n, 3, sk == SK_F || sk == SK_P);
+  if (smem > 227 * 1024) return fail(LRQ_ERUNTIME, "internal: cluster sweep needs too much shared memory");
+  int g = sm_count(s->device) & ~1;
+  const long long pairs = sp.num_tiles / 2;
+  if (pairs < g / 2) g = (int)(2 * pairs);
+  if (g < 2) return fail(LRQ_ERUNTIME, "internal: cluster sweep needs at least one tile pair");
+  switch (gk) {
+    case GK_C10: return launch_wdc_kind<GK_C10>(s->stream, sk, sp, g, smem);
+    case GK_C9: return launch_wdc_kind<GK_C9>(s->stream, sk, sp, g, smem);
+    case GK_C8: return launch_wdc_kind<GK_C8>(s->stream, sk, sp, g, smem);
+  }
+  return fail(LRQ_ERUNTIME, "internal: not a cluster group");
 }
 
 int launch_sweep(lrq_state* s, int gk, int sk, const SweepParams& sp_in, int grid) {
@@ -1793,6 +1863,19 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
         cpow_mul(sre, sim, f.qre, f.qim, g.ntargets);
         if (f.flip && (neg & 1)) sre = -sre, sim = -sim;
       }
+      if (g.cross >= 0) {
+        // the cross qubit of a cluster group: its tangents, and its sign in
+        // the (i s)^k factor of a flipped layer with per-qubit signs
+        for (int m = 0; m < 2; ++m) {
+          const int b = m == 0 ? w.beta1 : w.beta2;
+          sp.tc[m] = 0.0;
+          if (b < 0) continue;
+          const MixerForm f = mixer_form(mixer[b]);
+          const bool negq = signed_mix && s->msign_h[(size_t)b * n + g.cross] < 0;
+          sp.tc[m] = negq ? -f.t : f.t;
+          if (f.flip && negq) sre = -sre, sim = -sim;
+        }
+      }
       sp.scale_re = sre;
       sp.scale_im = sim;
       sp.init_re = init;
@@ -1815,7 +1898,9 @@ int lrq_run(lrq_state* s, int p, const double* phase, const double* mixer) {
       }
       char kname[2] = {"PMFRLQN"[w.kind], 0};
       NvtxRange nv_sweep(kname, group_name(g.kind));
-      int rc = w.prog == 1 ? launch_wd(s, g.kind, w.kind, sp) : launch_sweep(s, g.kind, w.kind, sp, grid);
+      int rc = w.prog == 2   ? launch_wdc(s, g.kind, w.kind, sp)
+               : w.prog == 1 ? launch_wd(s, g.kind, w.kind, sp)
+                             : launch_sweep(s, g.kind, w.kind, sp, grid);
       if (rc) return rc;
       record(s, ev++, "PMFRLQN"[w.kind]);
     }

@@ -27,10 +27,11 @@
 namespace lrq {
 
 struct PlanGroup {
-  int kind;        // GK_A / GK_H
+  int kind;        // GK_A / GK_H / GK_H4 / GK_C*
   int m, q0;       // tile amp bit i -> global i < m ? i : q0 + (i - m)
   unsigned tmask;  // tile amp bits that are mixer targets
-  int ntargets;
+  int ntargets;    // mixer targets of the group (a cluster group: + the cross qubit)
+  int cross = -1;  // cluster groups: the target qubit between the two CTAs' half tiles
 };
 
 struct PlanSweep {
@@ -58,7 +59,9 @@ struct Plan {
   std::vector<PlanSweep> sweeps;
 };
 
-inline std::vector<PlanGroup> plan_groups(int n, int pair) {
+inline std::vector<PlanGroup> plan_groups_tiles(int n, int pair);
+inline std::vector<PlanGroup> plan_groups(int n, int pair) { return plan_groups_tiles(n, pair); }
+inline std::vector<PlanGroup> plan_groups_tiles(int n, int pair) {
   const int KA = kUnitBits + pair;
   std::vector<PlanGroup> gs;
   PlanGroup a;
@@ -103,6 +106,48 @@ inline std::vector<PlanGroup> plan_groups(int n, int pair) {
   return gs;
 }
 
+// complex64 cluster-pair groups (lrq_sweep_wdc.cuh): for n - 13 in [16, 20]
+// the qubits above group A split into two groups of 8-10 targets whose
+// 128 KB tiles (two CTAs) have 128-512 B runs, instead of 64 / 128 B runs in
+// 64 KB tiles.  The group with the longer runs takes the top qubits (the
+// largest stride).  Opt-in ($LRQ_CLUSTER=1): measured on B200 the longer runs
+// do lift the copy ceiling of the tile pattern (5.8 vs 4.6 TB/s), but the
+// cluster kernels are issue/latency-bound at 22-24 ms per F sweep against
+// 15-16 ms for the single-CTA kernel.
+inline bool use_cluster_plan(int n, int pair) {
+  const char* v = getenv("LRQ_CLUSTER");
+  if (!(v && *v == '1')) return false;
+  const int rest = n - (kUnitBits + pair);
+  return pair == 1 && rest >= 16 && rest <= 20;
+}
+inline std::vector<PlanGroup> plan_groups_cluster(int n, int pair) {
+  const int KA = kUnitBits + pair;
+  std::vector<PlanGroup> gs;
+  PlanGroup a;
+  a.kind = GK_A;
+  a.m = KA;
+  a.q0 = KA;
+  a.tmask = (1u << KA) - 1u;
+  a.ntargets = KA;
+  gs.push_back(a);
+  const int rest = n - KA;
+  const int k_lo = rest / 2, k_hi = rest - k_lo;  // k_hi >= k_lo: more targets low, longer runs on top
+  const int ks[2] = {k_hi, k_lo};
+  int q = KA;
+  for (int k : ks) {
+    PlanGroup h;
+    h.kind = k == 10 ? GK_C10 : (k == 9 ? GK_C9 : GK_C8);
+    h.m = group_ma(h.kind, pair);  // = 14 - k
+    h.q0 = q;
+    h.tmask = ((1u << KA) - 1u) & ~((1u << h.m) - 1u);  // the k - 1 local targets
+    h.ntargets = k;
+    h.cross = q + k - 1;
+    gs.push_back(h);
+    q += k;
+  }
+  return gs;
+}
+
 // Butterfly masks come from the compile-time programs (prog_mask); a masked
 // register bit that is not one of the group's targets gets tangent 0.
 // mask*[r] = register amp bits that take a real butterfly in round r,
@@ -141,7 +186,7 @@ inline void plan_rounds_wd(const PlanGroup& g, int pair, PlanSweep& sw) {
 }
 
 inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
-  if (sw.prog == 1) {
+  if (sw.prog == 1 || sw.prog == 2) {
     plan_rounds_wd(g, pair, sw);
     return;
   }
@@ -171,7 +216,7 @@ inline void plan_rounds(const PlanGroup& g, int pair, PlanSweep& sw) {
 
 // global qubit behind tangent slot a of round r (the bit a of mask1/mask2)
 inline int sweep_qubit(const PlanGroup& g, const PlanSweep& w, int pair, int r, int a) {
-  const int tb = w.prog == 1 ? (wd_layout(w.kind, r) == 1 ? 7 : 2) + a + pair
+  const int tb = w.prog >= 1 ? (wd_layout(w.kind, r) == 1 ? 7 : 2) + a + pair
                              : reg_tile_bit(pair, prog_lo(g.kind, pair, w.kind, r), a);
   return tb < g.m ? tb : g.q0 + (tb - g.m);
 }
@@ -201,7 +246,8 @@ inline Plan make_plan(int n, int pair, int p) {
   P.KA = kUnitBits + pair;
   P.small = n < P.KA;
   if (P.small || p < 1) return P;
-  P.groups = plan_groups(n, pair);
+  const bool cluster = use_cluster_plan(n, pair);
+  P.groups = cluster ? plan_groups_cluster(n, pair) : plan_groups(n, pair);
   const int S = (int)P.groups.size();
   if (S >= 3) {
     // >= 2 high groups: the fused F sweeps go to the two end HIGH groups
@@ -219,10 +265,13 @@ inline Plan make_plan(int n, int pair, int p) {
     {
       const int first_last = (p == 1 || (p - 2) % 2 == 1) ? seq.front() : seq.back();
       const int other = first_last == seq.front() ? seq.back() : seq.front();
-      if (P.groups[other].kind == GK_H && P.groups[first_last].kind == GK_H4) std::reverse(seq.begin(), seq.end());
+      // (longer runs stream faster: H4 over H, C9 over C10)
+      if (P.groups[other].m < P.groups[first_last].m) std::reverse(seq.begin(), seq.end());
     }
     const char* nowd = getenv("LRQ_NO_WD");  // debugging: classic kernels, same order
     auto wd = [&](int gi, int kind) {
+      // cluster groups: every sweep on the cluster-pair kernel (prog 2)
+      if (is_cluster_group(P.groups[gi].kind)) return 2;
       // F only: a lone high-group M (last layer) streams faster on the classic TMA kernel
       return !(nowd && *nowd == '1') && P.groups[gi].kind != GK_A && (kind == SK_F || kind == SK_P) ? 1 : 0;
     };
@@ -360,8 +409,10 @@ inline std::string plan_json(const Plan& P) {
   for (size_t i = 0; i < P.groups.size(); ++i) {
     const PlanGroup& g = P.groups[i];
     s += (i ? "," : "");
-    s += "{\"kind\":\"" + std::string(g.kind == GK_A ? "A" : (g.kind == GK_H4 ? "H4" : "H")) + "\",\"m\":" + std::to_string(g.m) +
-         ",\"q0\":" + std::to_string(g.q0) + ",\"tmask\":" + std::to_string(g.tmask) + "}";
+    const char* kn = g.kind == GK_A ? "A" : g.kind == GK_H4 ? "H4" : g.kind == GK_C10 ? "C10" : g.kind == GK_C9 ? "C9"
+                     : g.kind == GK_C8 ? "C8" : "H";
+    s += "{\"kind\":\"" + std::string(kn) + "\",\"m\":" + std::to_string(g.m) + ",\"q0\":" + std::to_string(g.q0) +
+         ",\"tmask\":" + std::to_string(g.tmask) + ",\"cross\":" + std::to_string(g.cross) + "}";
   }
   s += "],\"sweeps\":[";
   for (size_t i = 0; i < P.sweeps.size(); ++i) {
@@ -374,7 +425,7 @@ inline std::string plan_json(const Plan& P) {
          ",\"reduce\":" + (w.reduce ? "true" : "false") + ",\"rounds\":[";
     for (int r = 0; r < w.nrounds; ++r) {
       s += (r ? "," : "");
-      if (w.prog == 1) {  // lo: the lowest register unit bit of the layout
+      if (w.prog >= 1) {  // lo: the lowest register unit bit of the layout
         const bool ph = (w.kind == SK_F && r == 1) || (w.kind == SK_P && r == 0);
         s += "[" + std::to_string(wd_layout(w.kind, r) == 1 ? 7 : 2) + "," + std::to_string(w.tmask1[r]) + "," +
              std::to_string(w.tmask2[r]) + "," + (ph ? "1" : "0") + ",0]";

@@ -36,7 +36,18 @@ constexpr int kThreads = 256;  // 8 thread bits + 4 register unit bits
 // 64 B) or 4 (c128, 256 B).  H4: complex64 runs of 16 amplitudes (128 B) for
 // the middle groups, which take a mixer-only sweep every layer: whole 128 B
 // lines keep twice the bytes in flight per outstanding L2 request.
-enum GroupKind { GK_A = 0, GK_H = 1, GK_H4 = 2 };
+enum GroupKind {
+  GK_A = 0,
+  GK_H = 1,
+  GK_H4 = 2,
+  // complex64 cluster-pair groups (lrq_sweep_wdc.cuh): a 128 KB tile over two
+  // CTAs, k targets with runs of 2^(14-k) amplitudes (C10: 128 B, C9: 256 B,
+  // C8: 512 B); the top target is the cross qubit between the two CTAs
+  GK_C10 = 3,
+  GK_C9 = 4,
+  GK_C8 = 5
+};
+__host__ __device__ constexpr bool is_cluster_group(int gk) { return gk >= GK_C10; }
 enum SweepKind {
   SK_P = 0,  // init, phase, mixer 2                         (first sweep)
   SK_M = 1,  // load, mixer 1, store                         (middle sweeps)
@@ -57,7 +68,11 @@ __host__ __device__ constexpr int layout_lo(int gk, int pair, int i) {
   return gk == GK_A ? (i == 0 ? 8 : (i == 1 ? 0 : 4)) : (i == 0 ? 8 : (i == 1 ? 4 : (gk == GK_H4 ? 3 : 2)));
 }
 __host__ __device__ constexpr int group_ma(int gk, int pair) {
-  return gk == GK_A ? 12 + pair : (gk == GK_H4 ? 4 : (pair ? 3 : 4));
+  return gk == GK_A ? 12 + pair
+         : gk == GK_C10 ? 4
+         : gk == GK_C9  ? 5
+         : gk == GK_C8  ? 6
+                        : (gk == GK_H4 ? 4 : (pair ? 3 : 4));
 }
 
 __host__ __device__ constexpr int prog_rounds(int gk, int pair, int sk) {
@@ -145,6 +160,7 @@ struct SweepParams {
   unsigned long long* red_arg;
   double* red_maxE;  // per-tile max E (may be null)
   int search;        // reductions: 1 = also min E with argmin (max-cut search) and max E
+  double tc[2];      // cluster groups: mixer tangents of the cross qubit (mixer 1, mixer 2; 0 = none)
   // p-weighted energy histogram (may be null): bin b = floor((E - hist_lo) *
   // hist_scale) clamped to [0, hist_bins); each amplitude adds round(p 2^60)
   // to its bin as a 64-bit integer, so the totals do not depend on the order

@@ -57,7 +57,7 @@ template <typename T, int GK, int SK>
 struct WdSweep {
   typedef typename UnitT<T>::U U;
   static constexpr int PAIR = UnitT<T>::PAIR;
-  static_assert(GK == GK_H || (GK == GK_H4 && PAIR), "warp-decoupled sweeps serve high groups");
+  static_assert(GK == GK_H || ((GK == GK_H4 || is_cluster_group(GK)) && PAIR), "warp-decoupled sweeps serve high groups");
   static constexpr int KA = kUnitBits + PAIR;
   static constexpr int RA = 5 + PAIR;         // register amp bits
   static constexpr int NV = 1 << RA;          // amplitudes per thread

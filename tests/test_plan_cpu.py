@@ -76,6 +76,8 @@ def emulate(plan, n, phase, mixer):
         g = groups[sw["group"]]
         m, q0, tmask = g["m"], g["q0"], g["tmask"]
         targets = [i if i < m else q0 + i - m for i in range(K) if (tmask >> i) & 1]
+        if g.get("cross", -1) >= 0:  # cluster group: the qubit between the two CTAs' half tiles
+            targets.append(g["cross"])
         assert all(0 <= q < n for q in targets)
         if sw["beta1"] >= 0:
             for q in targets:
@@ -125,6 +127,9 @@ def test_plan_structure(lib, n, pb):
         cover = []
         for g in groups:
             cover += [i if i < g["m"] else g["q0"] + i - g["m"] for i in range(K) if (g["tmask"] >> i) & 1]
+            if g.get("cross", -1) >= 0:
+                cover.append(g["cross"])
+                assert g["kind"] in ("C10", "C9", "C8") and pb == 8 and g["cross"] == g["q0"] + K - g["m"]
         assert sorted(cover) == list(range(n))
         S = len(groups)
         sweeps = plan["sweeps"]
@@ -136,7 +141,7 @@ def test_plan_structure(lib, n, pb):
             g = groups[sw["group"]]
             m1 = m2 = 0
             for lo, a, b, _, _ in sw["rounds"]:
-                assert lo in ((2, 7) if sw.get("prog") == 1 else (0, 2, 3, 4, 8))
+                assert lo in ((2, 7) if sw.get("prog") in (1, 2) else (0, 2, 3, 4, 8))
                 assert not (m1 & a) and not (m2 & b), "a target takes one butterfly per mixer"
                 m1 |= a
                 m2 |= b
@@ -150,6 +155,11 @@ def test_plan_structure(lib, n, pb):
                 # warp-decoupled high-group sweep (TMA in / out)
                 assert g["kind"] != "A" and sw["kind"] in "PMF" and (pair == 1 or g["kind"] == "H")
                 continue
+            if sw.get("prog") == 2:
+                # cluster-pair sweep (every sweep of a cluster group)
+                assert g["kind"] in ("C10", "C9", "C8") and sw["kind"] in "PMF"
+                continue
+            assert g.get("cross", -1) < 0
             for lo in {sw["rounds"][-1][0], sw["rounds"][0][0]}:
                 if g["kind"] == "A":
                     assert lo != 0
@@ -157,3 +167,29 @@ def test_plan_structure(lib, n, pb):
                     assert lo >= g["m"] - pair
         if n in (32,) and pb == 8:
             assert S == 3  # 2 HBM passes per layer for the bench workload
+
+
+@pytest.mark.parametrize("n", [29, 30, 31, 32, 33])
+def test_cluster_plan_structure(lib, n, monkeypatch):
+    """The opt-in cluster plan (LRQ_CLUSTER=1): group A plus two C groups of
+    8-10 targets (128 KB pair tiles, 128-512 B runs); every sweep of a C
+    group runs the cluster-pair kernel (prog 2); the cross qubit is the
+    group's top target."""
+    monkeypatch.setenv("LRQ_CLUSTER", "1")
+    plan = json.loads(_native.describe_plan(n, 8, 3))
+    groups = plan["groups"]
+    assert [g["kind"][0] for g in groups] == ["A", "C", "C"]
+    cover = []
+    for g in groups:
+        cover += [i if i < g["m"] else g["q0"] + i - g["m"] for i in range(13) if (g["tmask"] >> i) & 1]
+        if g["cross"] >= 0:
+            cover.append(g["cross"])
+            assert g["m"] == 14 - int(g["kind"][1:]) and g["cross"] == g["q0"] + 13 - g["m"]
+    assert sorted(cover) == list(range(n))
+    assert groups[1]["m"] <= groups[2]["m"]  # the longer runs on the top qubits
+    for sw in plan["sweeps"]:
+        assert (sw["prog"] == 2) == (sw["group"] != 0)
+    if n == 32:
+        assert [g["kind"] for g in groups] == ["A", "C10", "C9"]
+    monkeypatch.setenv("LRQ_CLUSTER", "0")
+    assert all(g["cross"] < 0 for g in json.loads(_native.describe_plan(n, 8, 3))["groups"])
