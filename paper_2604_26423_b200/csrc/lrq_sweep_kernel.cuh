@@ -122,12 +122,18 @@ struct SweepTile {
 
   template <bool SEARCH, bool HIST>
   __device__ static __forceinline__ void reduce_loop(Ctx& c, const SweepParams& P, const double (&Elo)[4],
-                                                     const double (&Ehi)[NV / 4], unsigned vmask, bool thread_ok,
+                                                     const double (&Fh)[3], unsigned vmask, bool thread_ok,
                                                      double& sp_, double& spe, double& mine, double& maxe,
                                                      int& bestv) {
+    double eh = 0.0;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const double ev = (Elo[v & 3] + Ehi[v >> 2]) + c.ERR[v];
+      if ((v & 3) == 0) {
+        const int h = v >> 2;
+        eh = ((h & 1) ? -Fh[0] : Fh[0]) + ((h & 2) ? -Fh[1] : Fh[1]);
+        if constexpr (RA == 5) eh += (h & 4) ? -Fh[2] : Fh[2];
+      }
+      const double ev = (Elo[v & 3] + eh) + c.ERR[v];
       if constexpr (AMPS) {
         const double pv = prob(amp_get(c.r, v));
         sp_ += pv;
@@ -166,15 +172,12 @@ struct SweepTile {
       if (S::gpos(i, c.q0) == P.min_bit) vmask = 1u << a;
     }
     if (P.min_bit == -2 || (P.min_bit >= 0 && ((c.base >> P.min_bit) & 1ull))) thread_ok = false;
-    double Elo[4], Ehi[NV / 4];
+    // E(v) = (Elo[v & 3] + Ehi(v >> 2)) + ERR[v]; Ehi is formed inside the
+    // loop (fewer live registers: the R kernel runs 2 CTAs per SM)
+    double Elo[4];
 #pragma unroll
     for (int l = 0; l < 4; ++l) Elo[l] = C + ((l & 1) ? -F[0] : F[0]) + ((l & 2) ? -F[1] : F[1]);
-#pragma unroll
-    for (int h = 0; h < NV / 4; ++h) {
-      double e = ((h & 1) ? -F[2] : F[2]) + ((h & 2) ? -F[3] : F[3]);
-      if constexpr (RA == 5) e += (h & 4) ? -F[4] : F[4];
-      Ehi[h] = e;
-    }
+    const double Fh[3] = {F[2], F[3], RA == 5 ? F[4] : 0.0};
     double sp_ = 0.0, spe = 0.0, mine = __longlong_as_double(0x7ff0000000000000ll);
     double maxe = -__longlong_as_double(0x7ff0000000000000ll);
     int bestv = NV;
@@ -182,14 +185,14 @@ struct SweepTile {
     // max-cut optimum already known), + min/argmin/max E search, + histogram
     if (!AMPS || P.search) {
       if (AMPS && c.shist)
-        reduce_loop<true, true>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+        reduce_loop<true, true>(c, P, Elo, Fh, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
       else
-        reduce_loop<true, false>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+        reduce_loop<true, false>(c, P, Elo, Fh, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
     } else {
       if (c.shist)
-        reduce_loop<false, true>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+        reduce_loop<false, true>(c, P, Elo, Fh, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
       else
-        reduce_loop<false, false>(c, P, Elo, Ehi, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
+        reduce_loop<false, false>(c, P, Elo, Fh, vmask, thread_ok, sp_, spe, mine, maxe, bestv);
     }
     unsigned long long zbest = ~0ull;
     if (bestv < NV) {
@@ -353,8 +356,18 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   U* gamps = reinterpret_cast<U*>(P.amps);
   const int bl = qU - MU;  // block unit bits below the high run
 
+  // per-launch scalars held in registers across the tile loop (a reload from
+  // the parameter bank after every barrier stalled the loop: the parameter
+  // block is larger than the constant cache); the empty asm keeps the
+  // compiler from re-materialising them as constant loads
+  // scale mode: 0 none, 1 real, 2 complex
+  int smode = (P.scale_re == 1.0 && P.scale_im == 0.0) ? 0 : (P.scale_im == 0.0 ? 1 : 2);
+  float sre32 = (float)P.scale_re;
+  unsigned ntile = (unsigned)P.num_tiles;
+  asm volatile("" : "+r"(smode), "+f"(sre32), "+r"(ntile));
   int par = 0;
-  for (long long tid = blockIdx.x; tid < P.num_tiles; tid += gridDim.x, par ^= 1) {
+  for (unsigned tid32 = blockIdx.x; tid32 < ntile; tid32 += gridDim.x, par ^= 1) {
+    const long long tid = tid32;
     const uint64_t ut = (uint64_t)tid;
     const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
     c.base = baseU << PAIR;
@@ -397,18 +410,22 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     c.ebbJ = EBB[par * 2 + 0];
     c.ebbW = EBB[par * 2 + 1];
     if constexpr (AMPS && !INIT && !HAS_PHASE) {
-      if (!(P.scale_re == 1.0 && P.scale_im == 0.0)) {
+      if (smode == 1) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           A x = amp_get(c.r, v);
-          if (P.scale_im == 0.0) {
-            x.x *= (T)P.scale_re;
-            x.y *= (T)P.scale_re;
+          if constexpr (PAIR) {
+            x.x *= sre32;
+            x.y *= sre32;
           } else {
-            x = cmul_amp(x, make_double2(P.scale_re, P.scale_im));
+            x.x *= P.scale_re;
+            x.y *= P.scale_re;
           }
           amp_set(c.r, v, x);
         }
+      } else if (smode == 2) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) amp_set(c.r, v, cmul_amp(amp_get(c.r, v), make_double2(P.scale_re, P.scale_im)));
       }
     }
 
