@@ -16,7 +16,9 @@ import numpy as np
 from .errors import AbortedRunError, CapacityError, StateError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblrq.so")
+# $LRQ_LIB selects another build of the same ABI (the bounds-checked
+# _lib/liblrq_checked.so of `python -m paper_2604_26423_b200.build --checked`)
+LIB_PATH = os.environ.get("LRQ_LIB") or os.path.join(_HERE, "_lib", "liblrq.so")
 ABI_VERSION = 2
 
 _lib = None

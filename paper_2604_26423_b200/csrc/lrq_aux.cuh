@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallParams P) {
   const int n = P.n, N = 1 << n;
   V* s = reinterpret_cast<V*>(smem);
   double* red = reinterpret_cast<double*>(s + N);  // 8 warps * 5
+  LRQ_CHECK_SMEM(smem, red + 5 * (blockDim.x >> 5));
   const int t = threadIdx.x;
   const int b = blockIdx.x;  // trajectory (batch); 0 for a single state
   const V* g0 = reinterpret_cast<const V*>(P.amps);
@@ -474,6 +475,7 @@ __device__ __forceinline__ void sample_one(const Src& src, int tile_bits, long l
     else lo = mid + 1;
   }
   const long long b = lo;
+  LRQ_CHECK(b >= 0 && b < T_tiles);
   const long long t0 = b << tile_bits;
   const long long L = (count - t0) < (1ll << tile_bits) ? (count - t0) : (1ll << tile_bits);
   const long long chunk = (L + 31) / 32;
@@ -505,6 +507,7 @@ __device__ __forceinline__ void sample_one(const Src& src, int tile_bits, long l
         break;
       }
     }
+    LRQ_CHECK(t0 + idx < count);
     *out = base_index + (unsigned long long)(t0 + idx);
   }
 }

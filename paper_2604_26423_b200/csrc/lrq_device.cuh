@@ -15,8 +15,37 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace lrq {
+
+// Checked build (build.py --checked, -DLRQ_CHECKED -> _lib/liblrq_checked.so):
+// device-side bounds and layout assertions in every kernel family; a failed
+// check prints its line and traps (a launch error, not a silent corruption).
+// The release build compiles them away.  This stands in for
+// compute-sanitizer, which the GPU pool does not run.
+#ifdef LRQ_CHECKED
+#define LRQ_CHECK(cond)                                                                          \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("LRQ_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define LRQ_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+// the carved shared-memory layout ends inside the dynamic allocation
+#define LRQ_CHECK_SMEM(base_raw, end_ptr) \
+  LRQ_CHECK((size_t)((const unsigned char*)(end_ptr) - (const unsigned char*)(base_raw)) <= dyn_smem_bytes())
 
 template <typename T> struct CxT;
 template <> struct CxT<float> { typedef float2 V; };

@@ -313,6 +313,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   double* ERR = reinterpret_cast<double*>(PRR32 + 32);
   double* rs = ERR + 32;
   unsigned long long* shist = reinterpret_cast<unsigned long long*>(rs + 5 * (kThreads / 32));
+  LRQ_CHECK_SMEM(smem, shist + (HAS_REDUCE && P.hist ? P.hist_bins : 0));
+  LRQ_CHECK(P.n <= 40 && q0 >= S::MA && (GK == GK_A || q0 + kUnitBits + PAIR - S::MA <= n));
   const bool hist = HAS_REDUCE && AMPS && P.hist != nullptr;
   if (hist)
     for (int i = t; i < P.hist_bins; i += kThreads) shist[i] = 0ull;
@@ -368,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
   int par = 0;
   for (unsigned tid32 = blockIdx.x; tid32 < ntile; tid32 += gridDim.x, par ^= 1) {
     const long long tid = tid32;
+    LRQ_CHECK(tid < P.num_tiles);
     const uint64_t ut = (uint64_t)tid;
     const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
     c.base = baseU << PAIR;

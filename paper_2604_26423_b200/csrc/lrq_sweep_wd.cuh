@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
   void* PRR = reinterpret_cast<void*>(thr + (kWdRAmax + 1) * kWdTT);  // NV phasors
   double* wsc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(PRR) + 16 * 64);  // per team
   int* blk = reinterpret_cast<int*>(wsc + kWdTeams * 16);  // the block (non-tile) bits
+  LRQ_CHECK_SMEM(smem_raw, blk + 64);
+  LRQ_CHECK(nst * kWdTeams <= 16 && n <= 40 && q0 + KA - MA <= n);
   int nb = 0;
   for (int j = 0; j < n; ++j)
     if (j >= MA && !(j >= q0 && j < q0 + KA - MA)) ++nb;
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
     U* rg = st + wq * kWdRegion;  // this warp's transpose region (after the team barrier)
     const uint64_t ut = (uint64_t)tid;
     const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
+    LRQ_CHECK((baseU << PAIR) < (1ull << n));
 
     if constexpr (PH) {
       // warp 0 of the team: per-tile fields on the tile bits from the fixed

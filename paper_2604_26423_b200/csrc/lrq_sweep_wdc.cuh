@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(TEAMS* kWdWarps * 32, 1) sweep_wdc_kernel(cons
   double* Tc = reinterpret_cast<double*>(blk + 64);   // [kWdTT] thread part of h_c
   float2* GRR = reinterpret_cast<float2*>(Tc + kWdTT);  // [64] exp(2 i s_c (register part of h_c))
   uint64_t* xbar = reinterpret_cast<uint64_t*>(GRR + 64);  // [team][warp][2]
+  LRQ_CHECK_SMEM(smem_raw, xbar + kWdcBarriers);
+  LRQ_CHECK((gridDim.x & 1) == 0 && cq < n && (P.num_tiles & 1) == 0);
   int nb = 0;
   for (int j = 0; j < n; ++j)
     if (j >= MA && !(j >= q0 && j < q0 + KA - MA)) ++nb;

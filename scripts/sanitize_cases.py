@@ -1,7 +1,10 @@
-"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck): every
-kernel family once at n = 14-16 (a few tiles), checked against the oracle.
+"""Small cases of every kernel family (n = 10-24, a few tiles each), checked
+against the oracle.  compute-sanitizer is closed on the GPU pool, so these run
+against the bounds-checked build instead (device asserts on tile indices,
+global extents and the carved shared-memory layouts):
 
-    compute-sanitizer --tool memcheck python scripts/sanitize_cases.py
+    python -m paper_2604_26423_b200.build --checked
+    LRQ_LIB=paper_2604_26423_b200/_lib/liblrq_checked.so python scripts/sanitize_cases.py
 """
 import os
 import sys
@@ -51,3 +54,10 @@ L.draw_indices(np.random.default_rng(0).random(5000), 100, L.derive_rng(0, "shot
 inst = L.generate_instance(13, 1)
 L.cut_values_range(inst, 0, 1 << 13)
 print("ok misc", flush=True)
+# the opt-in cluster-pair sweeps (complex64, n = 29: C8 + C8 groups)
+os.environ["LRQ_CLUSTER"] = "1"
+sv = L.run_circuit(L.build_circuit(L.generate_instance(29, 1), L.LrQaoaParams(p=2, delta_beta=0.9)), "fp32",
+                   memory_budget=1 << 40)
+print("ok cluster", sv.norm_squared(), flush=True)
+sv.release()
+os.environ["LRQ_CLUSTER"] = "0"

@@ -12,9 +12,14 @@ tot = Counter()
 cnt = Counter()
 samples = []
 stall_cols = [h for h in hdr if h.startswith("stall_") or "Stall" in h]
+seen = set()
 for r in data:
     if len(r) < len(hdr) or not r[ix["Instructions Executed"]].strip().isdigit():
         continue
+    if "Address" in ix:  # ncu lists each instruction once per view: count it once
+        if r[ix["Address"]] in seen:
+            continue
+        seen.add(r[ix["Address"]])
     src = r[ix["Source"]].strip()
     op = src.split()[0] if src else ""
     if op.startswith("@"):
