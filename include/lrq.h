@@ -179,6 +179,16 @@ int lrq_create_dist(int num_qubits, int precision_bytes, int device, int rank, i
                     uint64_t memory_budget, lrq_state **out);
 int lrq_dist_info(lrq_state *s, int *n_local, int *rank, int *world);
 
+/* An odd number of layers leaves a distributed state with its g global
+ * qubits and top g local qubits swapped (the run makes one remap per layer
+ * and no restoring one).  Reductions and sampling work in either layout;
+ * reading or writing the shard's amplitudes needs the identity layout:
+ * lrq_restore_layout (collective) makes the remaining remap and recomputes
+ * the reductions; lrq_copy_amps refuses a swapped shard.  layout_out of
+ * lrq_dist_layout: 0 identity, 1 swapped.                                 */
+int lrq_restore_layout(lrq_state *s);
+int lrq_dist_layout(lrq_state *s, int *layout_out);
+
 /* Remap transports over peer memory (NVLink).  Collective setup: every rank
  * exports its buffers (lrq_ipc_handles, LRQ_IPC_HANDLE_BYTES bytes), the host
  * gathers them in rank order (world * LRQ_IPC_HANDLE_BYTES bytes) and every

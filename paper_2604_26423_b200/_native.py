@@ -76,6 +76,8 @@ _SIGNATURES = {
     "lrq_ipc_handles": ([_state_p, _p, ctypes.c_size_t], _c_int),
     "lrq_fused_setup": ([_state_p, _p, ctypes.POINTER(_c_int)], _c_int),
     "lrq_dist_info": ([_state_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
+    "lrq_restore_layout": ([_state_p], _c_int),
+    "lrq_dist_layout": ([_state_p, ctypes.POINTER(_c_int)], _c_int),
     "lrq_describe_dist_plan": ([_c_int, _c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
     "lrq_dist_terms": ([_c_int, _c_int, _c_int, _c_int, _p, _p, _p, ctypes.POINTER(_c_dbl)], _c_int),
     "lrq_describe_remap": ([_c_int, _c_int, _c_int, ctypes.c_char_p, ctypes.c_size_t], _c_int),
@@ -372,6 +374,16 @@ class DeviceState:
         dt = np.complex64 if self.precision_bytes == 8 else np.complex128
         amps = np.ascontiguousarray(amps, dtype=dt)
         check(lib().lrq_store_amps(self.handle, int(start), int(amps.size), ptr(amps)))
+
+    def restore_layout(self) -> None:
+        """Collective on a distributed / shard state: the identity layout back
+        after an odd-p run (no-op otherwise)."""
+        check(lib().lrq_restore_layout(self.handle))
+
+    def layout(self) -> int:
+        v = _c_int(0)
+        check(lib().lrq_dist_layout(self.handle, ctypes.byref(v)))
+        return int(v.value)
 
     def set_search(self, on: bool) -> None:
         """Whether reducing passes search the max cut (min E, argmin, max E)."""

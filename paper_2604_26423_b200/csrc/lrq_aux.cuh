@@ -460,11 +460,12 @@ struct RawProb {
 template <typename Src>
 __device__ __forceinline__ void sample_one(const Src& src, int tile_bits, long long T_tiles, long long count,
                                            const double* __restrict__ prefix, double x, double goff, double gtotal,
-                                           unsigned long long base_index, unsigned long long* out) {
+                                           unsigned long long base_index, unsigned long long* out,
+                                           int write_unowned = 1) {
   const int lane = threadIdx.x & 31;
   const double total = gtotal;
   if (!(goff / total <= x && (goff + prefix[T_tiles]) / total > x)) {
-    if (lane == 0) *out = 0ull;
+    if (lane == 0 && write_unowned) *out = 0ull;  // one of several segments: leave the others' results
     return;
   }
   // first tile b with (goff + prefix[b+1]) / total > x
@@ -515,11 +516,12 @@ __device__ __forceinline__ void sample_one(const Src& src, int tile_bits, long l
 template <typename T>
 __global__ void sample_kernel(const void* amps_, int tile_bits, long long T_tiles, const double* __restrict__ prefix,
                               const double* __restrict__ u, long long shots, double goff, double gtotal,
-                              unsigned long long base_index, unsigned long long* __restrict__ out) {
+                              unsigned long long base_index, int write_unowned, unsigned long long* __restrict__ out) {
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (warp >= shots) return;
   AmpProb<T> src{reinterpret_cast<const typename CxT<T>::V*>(amps_)};
-  sample_one(src, tile_bits, T_tiles, T_tiles << tile_bits, prefix, u[warp], goff, gtotal, base_index, out + warp);
+  sample_one(src, tile_bits, T_tiles, T_tiles << tile_bits, prefix, u[warp], goff, gtotal, base_index, out + warp,
+             write_unowned);
 }
 
 // draw_indices over an explicit distribution (engine.py:254-263)

@@ -213,8 +213,14 @@ struct lrq_state {
   std::vector<cudaEvent_t> pev;    // world + 1 events: block j of the remap sweep done / remap done
   bool broken = false;             // a collective failed: the communicator was aborted
   std::vector<double> cost_edges;  // global cost edges (lexicographic)
-  double* dWx = nullptr;           // cost field from the rank's qubits (n_loc)
+  double* dWx = nullptr;           // cost field from the rank's qubits (n_loc), identity layout
   double wcst = 0.0;
+  // the cost in the swapped layout (global <-> top local qubits): the final
+  // pass of an odd-p run, and reductions before the layout is restored
+  double* dW1 = nullptr;
+  double* dWx1 = nullptr;
+  double wcst1 = 0.0;
+  int layout = 0;  // permutation state of the stored amplitudes (distributed states)
   double* dgather = nullptr;       // 4 * world doubles (all-gathered reductions)
   // optional per-layer Z fields / constant phases (lrq_run_fields)
   std::vector<double> field_h, cst_h;
@@ -263,6 +269,8 @@ void free_state(lrq_state* s) {
   cudaFree(s->didx);
   cudaFree(s->stage);
   cudaFree(s->dWx);
+  cudaFree(s->dW1);
+  cudaFree(s->dWx1);
   cudaFree(s->dF);
   cudaFree(s->dmsign);
   cudaFree(s->dgather);
@@ -1060,6 +1068,29 @@ int fused_barrier(lrq_state* s) {
   return LRQ_OK;
 }
 
+// A rank's view of the cost in permutation state `perm` and the local bit
+// that must be 0 in the max-cut search (the top logical qubit n-1: rank bit
+// g-1 in the identity layout, local bit n_loc-1 in the swapped one).
+MatArg cost_view(const lrq_state* s, int perm) {
+  MatArg W;
+  W.M = perm ? s->dW1 : s->dW;
+  W.ext = perm ? s->dWx1 : s->dWx;
+  W.cst = perm ? s->wcst1 : s->wcst;
+  return W;
+}
+int search_bit(const lrq_state* s, int perm) {
+  if (perm) return s->n - 1;
+  return ((s->rank >> (s->g - 1)) & 1) ? -2 : -1;
+}
+// global basis index of local index z on rank `rank` (n_loc local qubits),
+// in permutation `perm` (1: the top g local bits hold the global qubits and
+// the rank bits the qubits [n_loc-g, n_loc))
+uint64_t global_index(int nl, int g, int rank, int perm, uint64_t z) {
+  if (!perm) return ((uint64_t)rank << nl) | z;
+  const uint64_t low = z & ((1ull << (nl - g)) - 1ull), top = z >> (nl - g);
+  return low | ((uint64_t)rank << (nl - g)) | (top << nl);
+}
+
 // lrq_run for world > 1 (make_dist_plan): local sweeps in the permutation
 // state each one records, remaps between layers, final read-only reduction.
 int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
@@ -1089,9 +1120,6 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
   double* rmin = rpe + s->num_tiles;
   unsigned long long* rarg = reinterpret_cast<unsigned long long*>(rmin + s->num_tiles);
   double* rmax = rmin + 2 * s->num_tiles;
-  // the final pass runs in the identity permutation: the top logical qubit is
-  // rank bit g-1 (max-cut search over top bit 0)
-  const int min_bit = ((s->rank >> (g - 1)) & 1) ? -2 : -1;
   const Plan P = make_dist_plan(nl, g, pair_of(s->pbytes), p);
   const int grid_cap = 2 * sm_count(s->device);
   const int grid = (int)(s->num_tiles < grid_cap ? s->num_tiles : grid_cap);
@@ -1137,10 +1165,8 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
     sp.J.M = jm;
     sp.J.ext = w.phase >= 0 ? jm + (size_t)nl * nl : s->dzero;
     sp.J.cst = w.phase >= 0 ? cst[2 * w.phase + w.perm] : 0.0;
-    sp.W.M = s->dW;
-    sp.W.ext = s->dWx;
-    sp.W.cst = s->wcst;
-    sp.min_bit = min_bit;
+    sp.W = cost_view(s, w.perm);  // the final pass runs in the permutation the layers left
+    sp.min_bit = search_bit(s, w.perm);
     sp.red_p = rp;
     sp.red_pE = rpe;
     sp.red_minE = rmin;
@@ -1231,8 +1257,36 @@ int run_dist(lrq_state* s, int p, const double* phase, const double* mixer) {
   }
   s->ran = true;
   s->reduced = true;
+  s->layout = P.sweeps.back().perm;
   s->rank_sum_p.clear();
   return LRQ_OK;
+}
+
+// all ranks: `count` doubles from every rank (device buffer src), in rank order
+int gather_doubles(lrq_state* s, const double* src_dev, int count, std::vector<double>& h) {
+  if (s->group) {
+    lrq_group* G = s->group;
+    std::vector<double> mine((size_t)count);
+    CUDA_TRY(cudaMemcpyAsync(mine.data(), src_dev, sizeof(double) * count, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    {
+      std::lock_guard<std::mutex> lk(G->mu);
+      if (G->gather.size() < (size_t)count * G->world) G->gather.resize((size_t)count * G->world);
+      memcpy(&G->gather[(size_t)count * s->rank], mine.data(), sizeof(double) * count);
+    }
+    int rc = group_barrier(G);
+    if (rc) return rc;
+    {
+      std::lock_guard<std::mutex> lk(G->mu);
+      h.assign(G->gather.begin(), G->gather.begin() + (size_t)count * G->world);
+    }
+    return group_barrier(G);  // nobody overwrites a slot before all have read
+  }
+  if (!s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
+  NCCL_TRY_S(s, nccl().AllGather(src_dev, s->dgather, count, ncclDouble, s->comm, s->stream));
+  h.resize((size_t)count * s->world);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), s->dgather, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s->stream));
+  return dist_wait(s, s->stream);
 }
 
 // all ranks: the per-rank finalize scalars, gathered in rank order
@@ -1448,7 +1502,12 @@ int create_rank_state(int n_total, int pbytes, int device, int rank, int world, 
   cudaError_t e = staging ? cudaMalloc(&s->stage, s->chunk) : cudaSuccess;
   if (e == cudaSuccess) e = cudaMalloc(&s->dWx, sizeof(double) * nl);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->dWx, 0, sizeof(double) * nl, s->stream);
-  if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * kOutScalars * world);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dW1, sizeof(double) * nl * nl);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->dW1, 0, sizeof(double) * nl * nl, s->stream);
+  if (e == cudaSuccess) e = cudaMalloc(&s->dWx1, sizeof(double) * nl);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->dWx1, 0, sizeof(double) * nl, s->stream);
+  // all-gathered scalars: kOutScalars per rank, or world block masses per rank
+  if (e == cudaSuccess) e = cudaMalloc(&s->dgather, sizeof(double) * (kOutScalars + world) * world);
   if (e == cudaSuccess) e = cudaMalloc(&s->dflag, 2 * sizeof(float));
   if (e == cudaSuccess) e = cudaMemsetAsync(s->dflag, 0, 2 * sizeof(float), s->stream);
   if (e == cudaSuccess) e = cudaMalloc(&s->probe, sizeof(float) * world);
@@ -1686,6 +1745,12 @@ int lrq_create_shard(int n_total, int pbytes, int device, int rank, lrq_group* G
   return LRQ_OK;
 }
 
+int lrq_dist_layout(lrq_state* s, int* layout_out) {
+  if (!s || !layout_out) return fail(LRQ_EVALIDATION, "null argument");
+  *layout_out = s->layout;
+  return LRQ_OK;
+}
+
 int lrq_dist_info(lrq_state* s, int* n_local, int* rank, int* world) {
   if (!s) return fail(LRQ_EVALIDATION, "null state");
   if (n_local) *n_local = s->n;
@@ -1706,10 +1771,13 @@ int lrq_set_cost(lrq_state* s, const double* w) {
   DeviceGuard guard(s->device);
   if (s->world > 1) {
     // local view in the identity permutation (the final pass runs there)
-    std::vector<double> ext(n);
+    std::vector<double> ext(n), M1((size_t)n * n), ext1(n);
     s->cost_edges.assign(w, w + E);
     dist_terms(nt, s->g, s->rank, 0, w, M.data(), ext.data(), &s->wcst);
+    dist_terms(nt, s->g, s->rank, 1, w, M1.data(), ext1.data(), &s->wcst1);
     CUDA_TRY(cudaMemcpyAsync(s->dWx, ext.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->dW1, M1.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->dWx1, ext1.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
   } else {
     sym_matrix(n, w, M.data());
   }
@@ -2187,12 +2255,17 @@ int lrq_recompute(lrq_state* s) {
     sp.scale_re = 1.0;
     sp.J.M = s->dW;
     sp.J.ext = s->dzero;
-    sp.W.M = s->dW;
-    // a shard: the rank's field / constant, and the max-cut search over
-    // global top bit 0 (the state is in the identity permutation after a run)
-    sp.W.ext = s->world > 1 ? s->dWx : s->dzero;
-    sp.W.cst = s->world > 1 ? s->wcst : 0.0;
-    sp.min_bit = s->world > 1 ? (((s->rank >> (s->g - 1)) & 1) ? -2 : -1) : n - 1;
+    // a shard: the rank's cost view in the layout the state is in, and the
+    // max-cut search over global top bit 0
+    if (s->world > 1) {
+      sp.W = cost_view(s, s->layout);
+      sp.min_bit = search_bit(s, s->layout);
+    } else {
+      sp.W.M = s->dW;
+      sp.W.ext = s->dzero;
+      sp.W.cst = 0.0;
+      sp.min_bit = n - 1;
+    }
     sp.red_p = rp;
     sp.red_pE = rpe;
     sp.red_minE = rmin;
@@ -2240,7 +2313,7 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
       uint64_t z;
       memcpy(&z, &a[3], 8);
       if (z == ~0ull) continue;
-      const uint64_t gz = ((uint64_t)r << s->n) | z;
+      const uint64_t gz = global_index(s->n, s->g, r, s->layout, z);
       if (a[2] < mn || (a[2] == mn && gz < best)) {
         mn = a[2];
         best = gz;
@@ -2271,26 +2344,6 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   if (!s->reduced) return fail(LRQ_ERUNTIME, "no CDF: set a cost and run the circuit first");
   DeviceGuard guard(s->device);
   NvtxRange nv("lrq_sample");
-  double total = 0.0, off = 0.0;
-  unsigned long long base_index = 0;
-  if (s->world > 1) {
-    // global CDF over ranks in rank order: this rank owns the uniforms that
-    // land in [off, off + its mass) / total
-    if ((int)s->rank_sum_p.size() != s->world) {
-      lrq_reduction tmp;
-      int rc = lrq_reduce(s, &tmp);
-      if (rc) return rc;
-    }
-    for (int r = 0; r < s->world; ++r) {
-      if (r == s->rank) off = total;
-      total += s->rank_sum_p[r];
-    }
-    base_index = (unsigned long long)s->rank << s->n;
-  } else {
-    CUDA_TRY(cudaMemcpyAsync(&total, s->out, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    CUDA_TRY(cudaStreamSynchronize(s->stream));
-  }
-  if (!(total > 0.0)) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
   if (shots > s->shot_cap) {
     cudaFree(s->du);
     cudaFree(s->didx);
@@ -2300,19 +2353,82 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
     CUDA_TRY(cudaMalloc(&s->didx, sizeof(unsigned long long) * shots));
     s->shot_cap = shots;
   }
-  CUDA_TRY(cudaMemcpyAsync(s->du, u, sizeof(double) * shots, cudaMemcpyHostToDevice, s->stream));
   const int tile_bits = s->n < s->K ? s->n : s->K;
-  const long long threads = shots * 32;
-  const int block = 256;
-  const long long grid = (threads + block - 1) / block;
-  if (s->pbytes == 8)
-    sample_kernel<float><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
-                                                                   shots, off, total, base_index, s->didx);
-  else
-    sample_kernel<double><<<(unsigned)grid, block, 0, s->stream>>>(s->amps, tile_bits, s->num_tiles, s->prefix, s->du,
-                                                                    shots, off, total, base_index, s->didx);
-  CUDA_TRY(cudaGetLastError());
-  if (s->world > 1 && !s->group) {  // exactly one rank owns each shot; the others wrote 0
+  const long long grid = (shots * 32 + 255) / 256;
+  // one contiguous segment of the global CDF: tiles [t0, t0 + T) of this
+  // state starting at global cumulative mass goff, global indices base + local
+  auto segment = [&](long long t0, long long T, double goff, double total, unsigned long long base,
+                     int write_unowned) {
+    const void* amps = static_cast<const char*>(s->amps) + ((size_t)t0 << tile_bits) * s->pbytes;
+    if (s->pbytes == 8)
+      sample_kernel<float><<<(unsigned)grid, 256, 0, s->stream>>>(amps, tile_bits, T, s->prefix + t0, s->du, shots,
+                                                                  goff, total, base, write_unowned, s->didx);
+    else
+      sample_kernel<double><<<(unsigned)grid, 256, 0, s->stream>>>(amps, tile_bits, T, s->prefix + t0, s->du, shots,
+                                                                   goff, total, base, write_unowned, s->didx);
+    return cudaGetLastError();
+  };
+  CUDA_TRY(cudaMemcpyAsync(s->du, u, sizeof(double) * shots, cudaMemcpyHostToDevice, s->stream));
+  if (s->world > 1 && s->layout == 1) {
+    // swapped layout: global index order visits block b (top g local bits) of
+    // every rank in rank order, then block b+1: the CDF has world x world
+    // segments; each rank owns `world` of them.  The block masses come from
+    // the tile prefix, all-gathered; the uniforms in a segment are resolved
+    // by its owner and an integer sum gives every rank all indices.
+    const int G = s->world, g = s->g, nl = s->n;
+    const long long TB = s->num_tiles >> g;
+    std::vector<double> pre(G + 1);
+    for (int b = 0; b <= G; ++b)
+      CUDA_TRY(cudaMemcpyAsync(&pre[b], s->prefix + (size_t)b * TB, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    std::vector<double> mass(G);
+    for (int b = 0; b < G; ++b) mass[b] = pre[b + 1] - pre[b];
+    CUDA_TRY(cudaMemcpyAsync(s->dgather + (size_t)(kOutScalars + G) * G - G, mass.data(), sizeof(double) * G,
+                             cudaMemcpyHostToDevice, s->stream));
+    std::vector<double> all;  // all[r * G + b]
+    int rc = gather_doubles(s, s->dgather + (size_t)(kOutScalars + G) * G - G, G, all);
+    if (rc) {
+      if (s->group) group_abort(s->group, g_err);
+      return rc;
+    }
+    double total = 0.0;
+    for (int b = 0; b < G; ++b)
+      for (int r = 0; r < G; ++r) total += all[(size_t)r * G + b];
+    if (!(total > 0.0)) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
+    CUDA_TRY(cudaMemsetAsync(s->didx, 0, sizeof(unsigned long long) * shots, s->stream));
+    double off = 0.0;
+    for (int b = 0; b < G; ++b)
+      for (int r = 0; r < G; ++r) {
+        if (r == s->rank) {
+          const unsigned long long base = ((unsigned long long)b << nl) | ((unsigned long long)r << (nl - g));
+          CUDA_TRY(segment((long long)b * TB, TB, off - pre[b], total, base, 0));
+        }
+        off += all[(size_t)r * G + b];
+      }
+  } else {
+    double total = 0.0, off = 0.0;
+    unsigned long long base_index = 0;
+    if (s->world > 1) {
+      // global CDF over ranks in rank order: this rank owns the uniforms that
+      // land in [off, off + its mass) / total
+      if ((int)s->rank_sum_p.size() != s->world) {
+        lrq_reduction tmp;
+        int rc = lrq_reduce(s, &tmp);
+        if (rc) return rc;
+      }
+      for (int r = 0; r < s->world; ++r) {
+        if (r == s->rank) off = total;
+        total += s->rank_sum_p[r];
+      }
+      base_index = (unsigned long long)s->rank << s->n;
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(&total, s->out, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    if (!(total > 0.0)) return fail(LRQ_EVALIDATION, "statevector has zero norm, nothing to sample");
+    CUDA_TRY(segment(0, s->num_tiles, off, total, base_index, 1));
+  }
+  if (s->world > 1 && !s->group) {  // exactly one rank owns each shot; the others hold 0
     if (!s->comm) return fail(LRQ_ERUNTIME, "aborted run: the communicator was aborted");
     NCCL_TRY_S(s, nccl().AllReduce(s->didx, s->didx, shots, ncclUint64, ncclSum, s->comm, s->stream));
   }
@@ -2331,9 +2447,27 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   return LRQ_OK;
 }
 
+// the identity layout back after an odd-p run (the one remap the run did not
+// make); collective.  The reductions are recomputed in the new layout.
+int lrq_restore_layout(lrq_state* s) {
+  if (!s) return fail(LRQ_EVALIDATION, "null state");
+  if (s->world < 2 || s->layout == 0) return LRQ_OK;
+  DeviceGuard guard(s->device);
+  NvtxRange nv("lrq_restore_layout");
+  int rc = remap_exchange(s, false, -1);
+  if (rc) {
+    if (s->group) group_abort(s->group, g_err);
+    return rc;
+  }
+  s->layout = 0;
+  if (s->reduced) return lrq_recompute(s);
+  return LRQ_OK;
+}
+
 int lrq_store_amps(lrq_state* s, uint64_t start, uint64_t count, const void* host) {
   if (!s || (!host && count)) return fail(LRQ_EVALIDATION, "null argument");
   if (start + count > (1ull << s->n)) return fail(LRQ_EVALIDATION, "amplitude range out of bounds");
+  s->layout = 0;  // the caller writes identity-layout amplitudes
   DeviceGuard guard(s->device);
   CUDA_TRY(cudaMemcpyAsync((char*)s->amps + start * s->pbytes, host, count * s->pbytes, cudaMemcpyHostToDevice,
                            s->stream));
@@ -2346,6 +2480,8 @@ int lrq_store_amps(lrq_state* s, uint64_t start, uint64_t count, const void* hos
 int lrq_copy_amps(lrq_state* s, uint64_t start, uint64_t count, void* host) {
   if (!s || (!host && count)) return fail(LRQ_EVALIDATION, "null argument");
   if (start + count > (1ull << s->n)) return fail(LRQ_EVALIDATION, "amplitude range out of bounds");
+  if (s->layout != 0)
+    return fail(LRQ_ERUNTIME, "the shard is in the swapped layout of an odd-p run: call lrq_restore_layout (collective) first");
   DeviceGuard guard(s->device);
   CUDA_TRY(cudaMemcpyAsync(host, (const char*)s->amps + start * s->pbytes, count * s->pbytes, cudaMemcpyDeviceToHost,
                            s->stream));

@@ -336,7 +336,7 @@ inline Plan make_plan(int n, int pair, int p) {
 // the next sweep on Z starts with the mixer of the just-arrived qubits:
 //   layer 0:  P(Z) [init, phase_0, mix_0(Z)], M(others) mix_0, REMAP
 //   layer k:  F(Z) [mix_{k-1}(L'), phase_k, mix_k(Z)], M(others) mix_k, REMAP
-//   end:      M(Z) [mix_{p-1}(L')], (REMAP if the permutation is odd), Q(A)
+//   end:      M(Z) [mix_{p-1}(L')], Q(A) in the permutation the layers left
 // Each sweep records the permutation state it runs in (the phase terms
 // depend on it); two remaps restore the identity.
 inline Plan make_dist_plan(int n_loc, int g, int pair, int p) {
@@ -389,10 +389,14 @@ inline Plan make_dist_plan(int n_loc, int g, int pair, int p) {
   PlanSweep last = make_sweep(Z, SK_M, p - 1, -1, -1, false);
   last.target1 = lmask;
   last.perm = perm;
-  last.remap_after = perm == 1;
   P.sweeps.push_back(last);
+  // the final pass runs in whichever permutation the layers left (an odd p
+  // leaves the global and top local qubits swapped): no restoring remap.
+  // Reductions, max-cut argmin and the sampler map indices through the
+  // permutation; amplitude reads restore the identity layout on demand
+  // (lrq_restore_layout).
   PlanSweep q = make_sweep(0, SK_Q, -1, -1, -1, true);
-  q.perm = 0;
+  q.perm = perm;
   P.sweeps.push_back(q);
   // P and F sweeps of the (high) group Z run the warp-decoupled kernel
   const char* nowd = getenv("LRQ_NO_WD");

@@ -103,6 +103,10 @@ class DistStateVector:
         return ShotSet(self.num_qubits, self._draw(u), int(rng_seed), "noiseless")
 
     def local_amps(self) -> np.ndarray:
+        """This rank's shard (identity layout).  Collective when the run had
+        an odd p: the final pass ran in the swapped layout and the remaining
+        remap is made here (every rank must call it)."""
+        self._dev.restore_layout()
         return self._dev.copy_amps()
 
     def gather_amps(self):
@@ -127,6 +131,7 @@ class DistStateVector:
 
         from .engine import lqsv_create, lqsv_write_range
 
+        self._dev.restore_layout()
         if self.rank == 0:
             lqsv_create(path, self.num_qubits, self._precision)
         dist.barrier(group=self._group)

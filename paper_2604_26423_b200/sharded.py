@@ -151,9 +151,10 @@ def _flips(mixer: np.ndarray) -> int:
 
 def remap_volume(circuit: CircuitIR, plan: ShardPlan, precision: Precision | str = Precision.FP32) -> int:
     """Amplitudes this engine moves between shards over the run: one block
-    transpose per layer ((G-1)/G of the state), a restoring one when p is
-    odd, and a full mirror exchange when an odd number of layers took the
-    deferred-X mixer form."""
+    transpose per layer ((G-1)/G of the state) and a full mirror exchange
+    when an odd number of layers took the deferred-X mixer form.  (An odd p
+    leaves the state in the swapped layout; reading its amplitudes makes one
+    more transpose then, lrq_restore_layout.)"""
     precision = Precision.coerce(precision)
     layers = lower_circuit(circuit)
     p = int(layers.mixer.size)
@@ -266,16 +267,27 @@ class ShardedStateVector:
     def num_shards(self) -> int:
         return len(self._shards)
 
+    def _identity_layout(self) -> None:
+        """An odd-p run leaves the shards in the swapped layout (the final
+        pass ran there); amplitude reads need the remaining remap first."""
+        if any(s.layout() for s in self._shards):
+            _collective(self._group, self._shards, lambda r, d: d.restore_layout())
+
     def shard_amps(self, shard: int) -> np.ndarray:
+        self._identity_layout()
         return self._shards[shard].copy_amps()
 
     @property
     def amps(self) -> np.ndarray:
         if self._amps is None:
-            self._amps = np.concatenate([s.copy_amps() for s in self._shards])
+            self._identity_layout()
+            a = np.concatenate([s.copy_amps() for s in self._shards])
+            a.setflags(write=False)
+            self._amps = a
         return self._amps
 
     def _copy_range(self, start: int, count: int) -> np.ndarray:
+        self._identity_layout()
         L = 1 << self._shards[0].n_local
         parts = []
         while count > 0:
@@ -326,6 +338,7 @@ class ShardedStateVector:
         """LQSV dump written by every shard's thread into its own byte range."""
         from .engine import lqsv_create, lqsv_write_range
 
+        self._identity_layout()
         lqsv_create(path, self.num_qubits, self._precision)
         L = 1 << self._shards[0].n_local
         _collective(self._group, self._shards,

@@ -86,26 +86,49 @@ def _worker(rank, world, port, n, p, seed, q):
             if remap_after:
                 state = _exchange(state, rank, world, g)
                 remaps += 1
-        # final pass (identity permutation): sum p, sum p C on this shard
-        m, f, c = _native.dist_terms(n, g, rank, 0, w)
+        # final pass in the permutation the layers left (an odd p leaves the
+        # global and top local qubits swapped; no restoring remap)
+        perm = plan["dist"][-1][0]
+        m, f, c = _native.dist_terms(n, g, rank, perm, w)
         cut = 0.5 * (float(w.sum()) - _local_energy(nl, m, f, c))
         probs = (state.real ** 2 + state.imag ** 2)
         sums = torch.tensor([probs.sum(), probs @ cut], dtype=torch.float64)
         parts = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, sums)
-        # sampler: rank-partitioned inverse CDF (lrq_sample / sample_kernel)
-        mass = [float(x[0]) for x in parts]
-        total = sum(mass)
-        off = sum(mass[:rank])
+        # sampler (lrq_sample): the global CDF in index order is a list of
+        # contiguous local segments - the whole shard per rank in the
+        # identity layout; block b of every rank, b major, in the swapped one
+        L = 1 << (nl - g)
+        if perm == 0:
+            segs = [(r, 0, 1 << nl, r << nl) for r in range(world)]
+        else:
+            segs = [(r, b * L, L, (b << nl) | (r << (nl - g))) for b in range(world) for r in range(world)]
+        mine = [probs[lo:lo + cnt].sum() for (r, lo, cnt, _) in segs if r == rank]
+        allm = [torch.zeros(len(mine), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allm, torch.tensor(mine, dtype=torch.float64))
+        mass_of, k_of = {}, {}
+        for r in range(world):
+            k_of[r] = 0
+        for (r, lo, cnt, base) in segs:
+            mass_of[(r, lo)] = float(allm[r][k_of[r]])
+            k_of[r] += 1
+        total = sum(mass_of.values())
         u = O.shot_uniforms(1, 2000)
-        cum = off + np.cumsum(probs)
         idx = np.zeros(u.size, dtype=np.int64)
-        for k, x in enumerate(u):
-            if off / total <= x < (off + probs.sum()) / total:
-                j = int(np.searchsorted(cum / total, x, side="right"))
-                idx[k] = (rank << nl) + min(j, probs.size - 1)
+        off = 0.0
+        for (r, lo, cnt, base) in segs:
+            mass = mass_of[(r, lo)]
+            if r == rank:
+                cum = off + np.cumsum(probs[lo:lo + cnt])
+                for k, x in enumerate(u):
+                    if off / total <= x < (off + mass) / total:
+                        j = int(np.searchsorted(cum / total, x, side="right"))
+                        idx[k] = base + min(j, cnt - 1)
+            off += mass
         shots = torch.from_numpy(idx)
         dist.all_reduce(shots)
+        if perm == 1:  # lrq_restore_layout: the remaining remap, for the amplitudes
+            state = _exchange(state, rank, world, g)
         gathered = [torch.zeros(2 << nl, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(gathered, torch.from_numpy(state.view(np.float64).copy()))
         if rank == 0:
@@ -145,7 +168,7 @@ def test_distributed_plan_emulation_matches_oracle(world, n, p):
     assert sum_pc == pytest.approx(O.expected_cut(n, w, probs), rel=1e-12)
     ref = O.draw(probs, O.shot_uniforms(1, 2000))
     assert int(np.sum(shots.astype(np.uint64) != ref)) <= 1
-    assert remaps == p + (p % 2)  # one per layer, plus a restoring one if p is odd
+    assert remaps == p  # one per layer: an odd p's final pass runs in the swapped layout
 
 
 def test_dist_terms_reproduce_global_energy():
@@ -177,20 +200,21 @@ def test_dist_plan_validation():
     plan = json.loads(_native.describe_dist_plan(36, 3, 16, 3))
     kinds = [s["kind"] for s in plan["sweeps"]]
     assert kinds[0] == "P" and kinds[-1] == "Q"
-    assert sum(r for _, r, _ in plan["dist"]) == 4  # 3 layer remaps + 1 restoring
+    # 3 layer remaps; the final pass runs in the swapped layout (no 4th remap)
+    assert sum(r for _, r, _ in plan["dist"]) == 3 and plan["dist"][-1][0] == 1
 
 
 @pytest.mark.parametrize("n,g,B,p", [(32, 3, 8, 3), (34, 3, 16, 3), (30, 1, 8, 2), (29, 2, 16, 4), (36, 3, 16, 3)])
 def test_dist_plan_remap_follows_group_a_mixer(n, g, B, p):
     """The fused remap redirects the stores of the sweep before a remap; that
-    needs a group-A (contiguous-tile) mixer-only sweep there.  Every layer
-    remap has one; the restoring remap of an odd p follows the last mixer
-    sweep of another group and runs as an exchange."""
+    needs a group-A (contiguous-tile) mixer-only sweep there.  Every remap
+    has one (an odd p ends in the swapped layout instead of remapping back)."""
     plan = json.loads(_native.describe_dist_plan(n, g, B, p))
     before = [(sw["kind"], plan["groups"][sw["group"]]["kind"])
               for sw, (_, remap_after, _) in zip(plan["sweeps"], plan["dist"]) if remap_after]
-    assert len(before) == p + (p % 2)
-    assert all(b == ("M", "A") for b in before[:p])
+    assert len(before) == p  # no restoring remap: the final pass runs in the layout the layers left
+    assert all(b == ("M", "A") for b in before)
+    assert plan["dist"][-1][0] == p % 2
 
 
 @pytest.mark.parametrize("B", [8, 16])

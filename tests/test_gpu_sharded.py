@@ -273,3 +273,43 @@ def test_streamed_dump_per_shard_round_trips_byte_identically(tmp_path):
     np.testing.assert_array_equal(L.sample(back, 500, rng_seed=3).indices, L.sample(dense, 500, rng_seed=3).indices)
     for s in (sv, back, dense):
         s.release()
+
+
+@pytest.mark.parametrize("n,G,p,prec,dbeta", [(18, 4, 3, "fp64", 0.2), (17, 8, 1, "fp64", 0.9), (26, 2, 3, "fp32", 0.2),
+                                              (16, 2, 5, "fp64", 1.2)])
+def test_odd_p_final_pass_runs_in_the_swapped_layout(n, G, p, prec, dbeta):
+    """An odd p leaves the global and top local qubits swapped; the engine
+    makes no restoring remap: the fused final pass (sum p, sum pC, min/max E,
+    the histogram) and the sampler work in that layout - the sampler walks
+    the (block, rank) segments of the global CDF - and an amplitude read
+    makes the remaining remap.  Against the dense engine."""
+    inst = L.solve_instance(L.generate_instance(n, 8), limit=n)
+    circ = L.build_circuit(L.generate_instance(n, 8), L.LrQaoaParams(p=p, delta_beta=dbeta))
+    sv, rec = L.run_circuit_sharded(circ, L.plan_for_shard_count(n, G), prec)
+    dense = L.run_circuit(circ, prec)
+    try:
+        assert all(d.layout() == 1 for d in sv._shards)
+        assert sum(g.kind in "YWT" for g in rec.gates) == p
+        red, red_d = sv._reductions(None), dense.device_state.reduce()
+        tol = 1e-12 if prec == "fp64" else 1e-6
+        assert red.sum_p == pytest.approx(red_d.sum_p, rel=tol)
+        assert red.sum_p_cut == pytest.approx(red_d.sum_p_cut, rel=tol)
+        assert int(red.argmax_cut) == int(red_d.argmax_cut)
+        assert red.min_energy == pytest.approx(red_d.min_energy, rel=1e-12)
+        assert red.max_energy == pytest.approx(red_d.max_energy, rel=1e-12)
+        s_sh = L.sample(sv, 3000, rng_seed=4).indices
+        s_de = L.sample(dense, 3000, rng_seed=4).indices
+        assert int(np.sum(s_sh != s_de)) <= (2 if prec == "fp64" else 60)
+        d_sh = L.exact_cut_distribution(sv, inst, bins=256)
+        d_de = L.exact_cut_distribution(dense, inst, bins=256)
+        assert np.max(np.abs(d_sh.probs - d_de.probs)) < (1e-12 if prec == "fp64" else 1e-6)
+        assert all(d.layout() == 1 for d in sv._shards)  # still swapped: nothing read the amplitudes
+        got = sv.amps  # the remaining remap
+        assert all(d.layout() == 0 for d in sv._shards)
+        assert normwise(got, dense.amps.astype(np.complex128)) < (1e-12 if prec == "fp64" else 3e-6)
+        # reductions and samples after the restore are the same
+        assert L.exact_expected_r(sv, inst) == pytest.approx(L.exact_expected_r(dense, inst), rel=tol)
+        np.testing.assert_array_equal(L.sample(sv, 3000, rng_seed=4).indices, s_sh)
+    finally:
+        sv.release()
+        dense.release()

@@ -58,7 +58,7 @@ def test_remap_volume_vs_reference_volume(n, G, p, prec):
     inst = L.generate_instance(n, 1)
     circ = L.build_circuit(inst, L.LrQaoaParams(p=p))
     plan = L.plan_for_shard_count(n, G)
-    remaps = p + (p % 2)
+    remaps = p  # one per layer; an odd p ends in the swapped layout (no restoring remap)
     assert L.remap_volume(circ, plan, prec) == remaps * (G - 1) * (1 << n) // G
     # the per-layer remap moves far less than the reference's per-gate swaps
     assert L.remap_volume(circ, plan, prec) * 4 < L.exchange_volume(circ, plan)
