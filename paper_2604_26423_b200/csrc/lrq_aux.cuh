@@ -464,7 +464,8 @@ __device__ __forceinline__ void sample_one(const Src& src, int tile_bits, long l
                                            int write_unowned = 1) {
   const int lane = threadIdx.x & 31;
   const double total = gtotal;
-  if (!(goff / total <= x && (goff + prefix[T_tiles]) / total > x)) {
+  // this segment covers the cumulative mass [goff + prefix[0], goff + prefix[T_tiles])
+  if (!((goff + prefix[0]) / total <= x && (goff + prefix[T_tiles]) / total > x)) {
     if (lane == 0 && write_unowned) *out = 0ull;  // one of several segments: leave the others' results
     return;
   }

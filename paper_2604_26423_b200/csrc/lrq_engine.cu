@@ -2338,6 +2338,8 @@ int lrq_reduce(lrq_state* s, lrq_reduction* out) {
   return LRQ_OK;
 }
 
+int lrq_restore_layout(lrq_state* s);
+
 int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
   if (!s || !u || !idx) return fail(LRQ_EVALIDATION, "null argument");
   if (shots < 1) return fail(LRQ_EVALIDATION, "shot count must be positive, got " + std::to_string(shots));
@@ -2368,6 +2370,12 @@ int lrq_sample(lrq_state* s, const double* u, int64_t shots, uint64_t* idx) {
                                                                    goff, total, base, write_unowned, s->didx);
     return cudaGetLastError();
   };
+  if (s->world > 1 && s->layout == 1 && (s->num_tiles >> s->g) == 0) {
+    // blocks smaller than a tile (tiny shards): no per-block masses in the
+    // tile prefix; make the remaining remap (collective, like this call)
+    const int rc = lrq_restore_layout(s);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaMemcpyAsync(s->du, u, sizeof(double) * shots, cudaMemcpyHostToDevice, s->stream));
   if (s->world > 1 && s->layout == 1) {
     // swapped layout: global index order visits block b (top g local bits) of
