@@ -194,11 +194,13 @@ def nccl_unique_id() -> bytes:
 
 # One parked lrq_state per (n, precision, device): run_circuit in a loop then
 # reuses the HBM allocation instead of cudaFree/cudaMalloc of the whole state.
-# Only states up to _POOL_MAX_BYTES are parked (a parked 128 GiB state would
-# block every other allocation), and a failed allocation drains the pool and
-# retries once.
+# States of any size are parked (a 128 GiB n=33 state re-allocated every call
+# costs as much as a third of the circuit); every native call that allocates
+# device memory goes through _retry_capacity, which drains the pool and retries
+# once when the allocation fails, so a parked state never blocks this library.
+# Callers allocating HBM themselves call drain_pool() first.
 _POOL: dict = {}
-_POOL_MAX_BYTES = 64 << 30
+_POOL_MAX_BYTES = None
 
 
 def drain_pool() -> None:
@@ -206,6 +208,18 @@ def drain_pool() -> None:
     while _POOL:
         _, h = _POOL.popitem()
         lib().lrq_destroy(h)
+
+
+def _retry_capacity(rc_fn):
+    """check(rc_fn()); on an out-of-memory error with states parked, drain
+    the pool and call once more."""
+    try:
+        check(rc_fn())
+    except CapacityError:
+        if not _POOL:
+            raise
+        drain_pool()
+        check(rc_fn())
 
 
 class DeviceState:
@@ -225,13 +239,7 @@ class DeviceState:
             self.set_search(True)
             return
         h = _state_p()
-        try:
-            check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
-        except CapacityError:
-            if not _POOL:
-                raise
-            drain_pool()
-            check(lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
+        _retry_capacity(lambda: lib().lrq_create(n, precision_bytes, self.device, int(budget), ctypes.byref(h)))
         self._h = h
 
     @classmethod
@@ -247,7 +255,7 @@ class DeviceState:
         h = _state_p()
         idbuf = ctypes.create_string_buffer(nccl_id, 128)
         check(lib().lrq_create_dist(n, precision_bytes, self.device, rank, world, idbuf, int(budget),
-                                    ctypes.byref(h)))
+                                    ctypes.byref(h)))  # collective: no local retry
         self._h = h
         self.n_local = n - (int(world).bit_length() - 1)
         self._dist = True
@@ -263,8 +271,8 @@ class DeviceState:
         self.precision_bytes = precision_bytes
         self.device = int(device)
         h = _state_p()
-        check(lib().lrq_create_shard(n, precision_bytes, self.device, rank, group.handle, int(budget),
-                                     ctypes.byref(h)))
+        _retry_capacity(lambda: lib().lrq_create_shard(n, precision_bytes, self.device, rank, group.handle,
+                                                       int(budget), ctypes.byref(h)))
         self._h = h
         self.n_local = n - (group.world.bit_length() - 1)
         self._dist = True
@@ -300,7 +308,8 @@ class DeviceState:
         pool already holds one for this shape (or park=False)."""
         if self._h is not None and _lib is not None:
             key = (self.n, self.precision_bytes, self.device)
-            if park and key not in _POOL and (self.precision_bytes << self.n) <= _POOL_MAX_BYTES:
+            if park and key not in _POOL and (_POOL_MAX_BYTES is None
+                                              or (self.precision_bytes << self.n) <= _POOL_MAX_BYTES):
                 _POOL[key] = self._h
             else:
                 _lib.lrq_destroy(self._h)
@@ -320,7 +329,7 @@ class DeviceState:
     def run(self, phase: np.ndarray, mixer: np.ndarray) -> None:
         phase = np.ascontiguousarray(phase, dtype=np.float64)
         mixer = np.ascontiguousarray(mixer, dtype=np.float64)
-        check(lib().lrq_run(self.handle, int(mixer.size), ptr(phase), ptr(mixer)))
+        _retry_capacity(lambda: lib().lrq_run(self.handle, int(mixer.size), ptr(phase), ptr(mixer)))
 
     def run_fields(self, phase: np.ndarray, field: np.ndarray, constant: np.ndarray, mixer: np.ndarray) -> None:
         """run() with per-layer single-Z fields (p x n) and constant phases (p)."""
@@ -331,13 +340,13 @@ class DeviceState:
         p = int(mixer.size)
         if field.size != p * self.n or constant.size != p:
             raise ValidationError(f"fields need shape ({p}, {self.n}) and constants ({p},)")
-        check(lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
+        _retry_capacity(lambda: lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
 
     def run_ex(self, phase: np.ndarray, mixer_q: np.ndarray) -> None:
         """run() with per-qubit mixer half-angles (p, n), equal up to sign per layer."""
         phase = np.ascontiguousarray(phase, dtype=np.float64)
         mixer_q = np.ascontiguousarray(mixer_q, dtype=np.float64)
-        check(lib().lrq_run_ex(self.handle, int(mixer_q.shape[0]), ptr(phase), ptr(mixer_q)))
+        _retry_capacity(lambda: lib().lrq_run_ex(self.handle, int(mixer_q.shape[0]), ptr(phase), ptr(mixer_q)))
 
     def permute_xor(self, mask: int) -> None:
         check(lib().lrq_permute_xor(self.handle, int(mask)))
@@ -346,11 +355,11 @@ class DeviceState:
         check(lib().lrq_reset(self.handle, int(which)))
 
     def apply_gate(self, kind: int, q0: int, q1: int = 0, theta: float = 0.0) -> None:
-        check(lib().lrq_apply_gate(self.handle, int(kind), int(q0), int(q1), float(theta)))
+        _retry_capacity(lambda: lib().lrq_apply_gate(self.handle, int(kind), int(q0), int(q1), float(theta)))
 
     def reduce(self) -> Reduction:
         r = Reduction()
-        check(lib().lrq_reduce(self.handle, ctypes.byref(r)))
+        _retry_capacity(lambda: lib().lrq_reduce(self.handle, ctypes.byref(r)))
         return r
 
     def recompute(self) -> None:
@@ -359,7 +368,7 @@ class DeviceState:
     def sample(self, u: np.ndarray) -> np.ndarray:
         u = np.ascontiguousarray(u, dtype=np.float64)
         out = np.empty(u.size, dtype=np.uint64)
-        check(lib().lrq_sample(self.handle, ptr(u), u.size, ptr(out)))
+        _retry_capacity(lambda: lib().lrq_sample(self.handle, ptr(u), u.size, ptr(out)))
         return out
 
     def copy_amps(self, start: int = 0, count: int | None = None) -> np.ndarray:
@@ -391,7 +400,7 @@ class DeviceState:
 
     def set_histogram(self, bins: int, lo: float = 0.0, hi: float = 1.0) -> None:
         """p-weighted E histogram of the next reducing pass (bins = 0: off)."""
-        check(lib().lrq_set_histogram(self.handle, int(bins), float(lo), float(hi)))
+        _retry_capacity(lambda: lib().lrq_set_histogram(self.handle, int(bins), float(lo), float(hi)))
         self.hist_bins = int(bins)
 
     def histogram(self) -> np.ndarray:
@@ -461,7 +470,8 @@ def cut_values(n: int, w: np.ndarray, z: np.ndarray | None = None, start: int = 
         count = z.size
     out = np.empty(count, dtype=np.float64)
     if count:
-        check(lib().lrq_cut_values(n, ptr(w), ptr(z) if z is not None else None, start, count, ptr(out), dev))
+        _retry_capacity(lambda: lib().lrq_cut_values(n, ptr(w), ptr(z) if z is not None else None, start, count,
+                                                     ptr(out), dev))
     return out
 
 
@@ -472,7 +482,8 @@ def cut_values_spin(n: int, w: np.ndarray, half_total: float, start: int, count:
     dev = default_device() if device is None else device
     out = np.empty(int(count), dtype=np.float64)
     if count:
-        check(lib().lrq_cut_values_spin(n, ptr(w), float(half_total), int(start), int(count), ptr(out), dev))
+        _retry_capacity(lambda: lib().lrq_cut_values_spin(n, ptr(w), float(half_total), int(start), int(count),
+                                                          ptr(out), dev))
     return out
 
 
@@ -483,7 +494,8 @@ def expected_cut_chunks(n: int, w: np.ndarray, half_total: float, probs: np.ndar
     probs = np.ascontiguousarray(probs, dtype=np.float64)
     dev = default_device() if device is None else device
     out = np.empty(max(1, probs.size >> 16), dtype=np.float64)
-    check(lib().lrq_expected_cut(n, ptr(w), float(half_total), ptr(probs), probs.size, ptr(out), dev))
+    _retry_capacity(lambda: lib().lrq_expected_cut(n, ptr(w), float(half_total), ptr(probs), probs.size, ptr(out),
+                                                   dev))
     return out
 
 
@@ -493,7 +505,7 @@ def draw_indices(probs: np.ndarray, u: np.ndarray, device: int | None = None) ->
     u = np.ascontiguousarray(u, dtype=np.float64)
     dev = default_device() if device is None else device
     out = np.empty(u.size, dtype=np.uint64)
-    check(lib().lrq_draw_indices(ptr(probs), probs.size, ptr(u), u.size, ptr(out), dev))
+    _retry_capacity(lambda: lib().lrq_draw_indices(ptr(probs), probs.size, ptr(u), u.size, ptr(out), dev))
     return out
 
 
@@ -502,7 +514,7 @@ def max_cut(n: int, w: np.ndarray, device: int | None = None):
     dev = default_device() if device is None else device
     z = _c_u64(0)
     v = _c_dbl(0.0)
-    check(lib().lrq_max_cut(n, ptr(w), dev, ctypes.byref(z), ctypes.byref(v)))
+    _retry_capacity(lambda: lib().lrq_max_cut(n, ptr(w), dev, ctypes.byref(z), ctypes.byref(v)))
     return int(z.value), float(v.value)
 
 
@@ -522,7 +534,7 @@ def noisy_batch(n: int, precision_bytes: int, phase: np.ndarray, mixer: np.ndarr
     if shots:
         u = np.ascontiguousarray(u, dtype=np.float64)
         idx = np.empty((T, shots), dtype=np.uint64)
-    check(lib().lrq_noisy_batch(n, precision_bytes, dev, T, p, ptr(phase), ptr(mixer), ptr(xmask), shots,
+    _retry_capacity(lambda: lib().lrq_noisy_batch(n, precision_bytes, dev, T, p, ptr(phase), ptr(mixer), ptr(xmask), shots,
                                 ptr(u) if shots else None, ptr(probs) if probs is not None else None,
                                 ptr(idx) if idx is not None else None))
     return probs, idx
