@@ -199,17 +199,22 @@ struct SweepTile {
       const int eU = S::ebase(c.t, lo) | ((bestv >> PAIR) << lo);
       zbest = c.base + (S::gunit(eU, c.qU) << PAIR) + (uint64_t)(bestv & PAIR);
     }
+    // without the search the extremes are the constants set above: only the
+    // two sums need the warp reduction
+    const bool full = !AMPS || P.search;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       sp_ += __shfl_xor_sync(0xffffffffu, sp_, o);
       spe += __shfl_xor_sync(0xffffffffu, spe, o);
-      const double om = __shfl_xor_sync(0xffffffffu, mine, o);
-      const unsigned long long oz = __shfl_xor_sync(0xffffffffu, zbest, o);
-      if (om < mine || (om == mine && oz < zbest)) {
-        mine = om;
-        zbest = oz;
+      if (full) {
+        const double om = __shfl_xor_sync(0xffffffffu, mine, o);
+        const unsigned long long oz = __shfl_xor_sync(0xffffffffu, zbest, o);
+        if (om < mine || (om == mine && oz < zbest)) {
+          mine = om;
+          zbest = oz;
+        }
+        maxe = fmax(maxe, __shfl_xor_sync(0xffffffffu, maxe, o));
       }
-      maxe = fmax(maxe, __shfl_xor_sync(0xffffffffu, maxe, o));
     }
     const int warp = c.t >> 5;
     if ((c.t & 31) == 0) {
@@ -226,6 +231,7 @@ struct SweepTile {
       for (int w = 0; w < kThreads / 32; ++w) {
         s0 += c.rs[w * 5 + 0];
         s1 += c.rs[w * 5 + 1];
+        if (!full) continue;
         const double om = c.rs[w * 5 + 2];
         const unsigned long long oz = (unsigned long long)__double_as_longlong(c.rs[w * 5 + 3]);
         if (om < mn || (om == mn && oz < zb)) {
