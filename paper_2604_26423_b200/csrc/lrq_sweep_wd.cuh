@@ -48,7 +48,7 @@ __host__ __device__ inline size_t wd_smem_bytes(int n, int nst, bool usesJ) {
   if (usesJ) b = align16(b + 8 * (size_t)(n * n + n));
   b += 8 * (size_t)((kWdRAmax + 1) * kWdTT);  // per-tile-thread constants
   b += 16 * 64;                               // PRR (float2 x 64 or double2 x 32)
-  b += 8 * (size_t)(kWdTeamsMax * 16);  // per-team hb[13] + ebb
+  b += 8 * (size_t)(kWdTeamsMax * 20);  // per team: hb[16] fields + 4 warp partials of the block energy
   b += 4 * 64;                         // block-bit list
   return align16(b) + 1024;
 }
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
   double* thr = reinterpret_cast<double*>(sp);                          // [RA+1][kWdTT]
   void* PRR = reinterpret_cast<void*>(thr + (kWdRAmax + 1) * kWdTT);  // NV phasors
   double* wsc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(PRR) + 16 * 64);  // per team
-  int* blk = reinterpret_cast<int*>(wsc + kWdTeams * 16);  // the block (non-tile) bits
+  int* blk = reinterpret_cast<int*>(wsc + kWdTeams * 20);  // the block (non-tile) bits
   LRQ_CHECK_SMEM(smem_raw, blk + 64);
   LRQ_CHECK(nst * kWdTeams <= 16 && n <= 40 && q0 + KA - MA <= n);
   int nb = 0;
@@ -297,6 +297,46 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
     }
   }
   __syncthreads();
+  // The per-tile fields only need the couplings of the block bits: compact
+  // tables over the Jm region (they are smaller), so that every warp of a
+  // team computes a share of them per tile with independent loads
+  //   rowA[m][i] = J[g_i][blk_m] (i < 16), Jb[j][m] = J[blk_j][blk_m],
+  //   Jxb[j] = ext[blk_j], gJx[i] = ext[g_i]
+  double *rowA = Jm, *Jb = nullptr, *Jxb = nullptr, *gJx = nullptr;
+  if (PH) {
+    Jb = rowA + nb * 16;
+    Jxb = Jb + nb * nb;
+    gJx = Jxb + nb;
+    const int total = nb * 16 + nb * nb + nb + 16;
+    constexpr int kMaxPer = 8;
+    LRQ_CHECK(total <= kMaxPer * kWdThreads && total <= n * n + n);
+    double vals[kMaxPer];
+#pragma unroll
+    for (int r = 0; r < kMaxPer; ++r) {
+      const int e = threadIdx.x + r * kWdThreads;
+      double v = 0.0;
+      if (e < nb * 16) {
+        const int m = e >> 4, i = e & 15;
+        v = i < KA ? Jm[W::gpos(i, q0) * n + blk[m]] : 0.0;
+      } else if (e < nb * 16 + nb * nb) {
+        const int e2 = e - nb * 16, j = e2 / nb, m = e2 - j * nb;
+        v = Jm[blk[j] * n + blk[m]];
+      } else if (e < nb * 16 + nb * nb + nb) {
+        v = Jx[blk[e - nb * 16 - nb * nb]];
+      } else if (e < total) {
+        const int i = e - nb * 16 - nb * nb - nb;
+        v = i < KA ? Jx[W::gpos(i, q0)] : 0.0;
+      }
+      vals[r] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kMaxPer; ++r) {
+      const int e = threadIdx.x + r * kWdThreads;
+      if (e < total) rowA[e] = vals[r];
+    }
+  }
+  __syncthreads();
 
   // refill: the thread that stores a tile loads the tile nst steps ahead
   // into its stage (no producer warp: 8 warps keep 255 registers).  P loads
@@ -326,8 +366,7 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
 
   const int team = warp / kWdWarps, wq = warp % kWdWarps;
   const int tt2 = wq | (lane << 2);  // tile-thread index in the phase layout (L2)
-  double* hb = wsc + team * 16;      // team: hb[0..KA-1] fields, hb[15] block energy
-  U* gamps = reinterpret_cast<U*>(P.amps);
+  double* hb = wsc + team * 20;      // team: hb[0..KA-1] fields, hb[16..19] warp partials of the block energy
   U r[32];
   constexpr int RPH = INIT ? 0 : 1;  // round of the phase / L2 layout
   const double2 scale = make_double2(P.scale_re, P.scale_im);
@@ -339,31 +378,52 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
     U* st = reinterpret_cast<U*>(stages + (size_t)s * kWdStageBytes);
     U* rg = st + wq * kWdRegion;  // this warp's transpose region (after the team barrier)
     const uint64_t ut = (uint64_t)tid;
+#ifdef LRQ_CHECKED
     const uint64_t baseU = ((ut & ((1ull << bl) - 1ull)) << MU) | ((ut >> bl) << (qU + kUnitBits - MU));
     LRQ_CHECK((baseU << PAIR) < (1ull << n));
+#endif
 
     if constexpr (PH) {
-      // warp 0 of the team: per-tile fields on the tile bits from the fixed
-      // (block) bits and the block bits' own energy, for the whole team
-      // (read after the team barrier below)
-      if (wq == 0) {
-        const uint64_t base = baseU << PAIR;
-        if (lane < KA) {
-          const int gi = W::gpos(lane, q0);
-          double acc = Jx[gi];
-          for (int m = 0; m < nb; ++m) acc = fma(Jm[gi * n + blk[m]], spin(base, blk[m]), acc);
-          hb[lane] = acc;
-        }
-        double term = 0.0;
-        for (int m = lane; m < nb; m += 32) {
-          const int j = blk[m];
-          double fj = 0.0;
-          for (int m2 = 0; m2 < nb; ++m2) fj = fma(Jm[j * n + blk[m2]], spin(base, blk[m2]), fj);
-          term += spin(base, j) * (Jx[j] + 0.5 * fj);
+      // per-tile fields on the tile bits from the block bits, and the block
+      // bits' own energy (read after the team barrier below); bit m of the
+      // tile index is block bit blk[m].  P (no loads: the fields are on the
+      // critical path) shares them among the team's 4 warps: fields
+      // i = 4 wq + lane / 8 with the block bits split mod 8 over 8 lanes, the
+      // energy's pairs j < m split mod 4 by warp.  M / F leave them to warp 0:
+      // the other team's warps issue while this team waits at its barrier,
+      // and spreading the work measured slower there.
+      if constexpr (INIT) {
+        const int i = 4 * wq + (lane >> 3), mm = lane & 7;
+        double a = 0.0;
+        for (int m = mm; m < nb; m += 8) a = fma(rowA[m * 16 + (i & 15)], spin(ut, m), a);
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 4);
+        if (mm == 0 && i < KA) hb[i] = gJx[i] + a;
+        double tq = 0.0;
+        for (int j = lane; j < nb; j += 32) {
+          double q = wq == 0 ? Jxb[j] : 0.0;
+          for (int m = j + 1 + wq; m < nb; m += kWdWarps) q = fma(Jb[j * nb + m], spin(ut, m), q);
+          tq = fma(spin(ut, j), q, tq);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
-        if (lane == 0) hb[15] = P.J.cst + term;
+        for (int o = 16; o > 0; o >>= 1) tq += __shfl_xor_sync(0xffffffffu, tq, o);
+        if (lane == 0) hb[16 + wq] = tq;
+      } else if (wq == 0) {
+        if (lane < KA) {
+          double a = gJx[lane];
+          for (int m = 0; m < nb; ++m) a = fma(rowA[m * 16 + lane], spin(ut, m), a);
+          hb[lane] = a;
+        }
+        double tq = 0.0;
+        for (int j = lane; j < nb; j += 32) {
+          double q = Jxb[j];
+          for (int m = j + 1; m < nb; ++m) q = fma(Jb[j * nb + m], spin(ut, m), q);
+          tq = fma(spin(ut, j), q, tq);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tq += __shfl_xor_sync(0xffffffffu, tq, o);
+        if (lane < 4) hb[16 + lane] = lane == 0 ? tq : 0.0;
       }
     }
 
@@ -386,12 +446,12 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
       for (int a = 0; a < 32; ++a) r[a] = rg[W::slot(a, lane)];
       W::template mix<W::L2MASK>(r, P.tf[0][1], P.td[0][1]);
     } else {
-      team_sync_n(1 + team, kWdWarps * 32);  // warp 0's tile fields are visible
+      team_sync_n(1 + team, kWdWarps * 32);  // the tile fields are visible
     }
 
     if constexpr (PH) {
       // phase in L2: E = C + sum_a s_a F_a + E_RR(v)
-      double C = hb[15] + thr[RA * kWdTT + tt2];
+      double C = (P.J.cst + ((hb[16] + hb[17]) + (hb[18] + hb[19]))) + thr[RA * kWdTT + tt2];
 #pragma unroll
       for (int j = 0; j < 7; ++j) {
         const double h = hb[W::thr_bit(2, j)];
@@ -420,7 +480,7 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
     for (int b = 0; b < 32; ++b) st[W::nat(wq, lane, b)] = r[b];
     fence_proxy_async();
     team_sync_n(1 + team, kWdWarps * 32);
-    if (wq == kWdWarps - 1 && lane == 0) {  // the last warp stores (warp 0 computes the next tile's fields)
+    if (wq == kWdWarps - 1 && lane == 0) {  // the last warp stores
       const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
       tma_store_5d(&P.tmap, st, 0, 0, c1, 0, c4);
       bulk_commit();
