@@ -302,8 +302,11 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
   // team computes a share of them per tile with independent loads
   //   rowA[m][i] = J[g_i][blk_m] (i < 16), Jb[j][m] = J[blk_j][blk_m],
   //   Jxb[j] = ext[blk_j], gJx[i] = ext[g_i]
+  // (complex128 P keeps the direct form below: the tables' extra pointers
+  // spill at its 168 registers, +3 % measured)
+  constexpr bool TABLES = PH && !(INIT && !PAIR);
   double *rowA = Jm, *Jb = nullptr, *Jxb = nullptr, *gJx = nullptr;
-  if (PH) {
+  if (TABLES) {
     Jb = rowA + nb * 16;
     Jxb = Jb + nb * nb;
     gJx = Jxb + nb;
@@ -386,13 +389,14 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
     if constexpr (PH) {
       // per-tile fields on the tile bits from the block bits, and the block
       // bits' own energy (read after the team barrier below); bit m of the
-      // tile index is block bit blk[m].  P (no loads: the fields are on the
-      // critical path) shares them among the team's 4 warps: fields
-      // i = 4 wq + lane / 8 with the block bits split mod 8 over 8 lanes, the
-      // energy's pairs j < m split mod 4 by warp.  M / F leave them to warp 0:
-      // the other team's warps issue while this team waits at its barrier,
-      // and spreading the work measured slower there.
-      if constexpr (INIT) {
+      // tile index is block bit blk[m].  Complex64 P (no loads: the fields
+      // are on the critical path) shares them among the team's 4 warps:
+      // fields i = 4 wq + lane / 8 with the block bits split mod 8 over 8
+      // lanes, the energy's pairs j < m split mod 4 by warp.  The others leave
+      // them to warp 0: the other team's warps issue while this team waits at
+      // its barrier, and spreading the work measured slower there
+      // (profiles/r02_ab_tile_fields.txt).
+      if constexpr (INIT && PAIR) {
         const int i = 4 * wq + (lane >> 3), mm = lane & 7;
         double a = 0.0;
         for (int m = mm; m < nb; m += 8) a = fma(rowA[m * 16 + (i & 15)], spin(ut, m), a);
@@ -409,6 +413,27 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tq += __shfl_xor_sync(0xffffffffu, tq, o);
         if (lane == 0) hb[16 + wq] = tq;
+      } else if (!TABLES) {
+        if (wq == 0) {
+          const uint64_t base = ((ut & ((1ull << bl) - 1ull)) << (MU + PAIR)) |
+                                ((ut >> bl) << (qU + kUnitBits - MU + PAIR));
+          if (lane < KA) {
+            const int gi = W::gpos(lane, q0);
+            double acc = Jx[gi];
+            for (int m = 0; m < nb; ++m) acc = fma(Jm[gi * n + blk[m]], spin(base, blk[m]), acc);
+            hb[lane] = acc;
+          }
+          double term = 0.0;
+          for (int m = lane; m < nb; m += 32) {
+            const int j = blk[m];
+            double fj = 0.0;
+            for (int m2 = 0; m2 < nb; ++m2) fj = fma(Jm[j * n + blk[m2]], spin(base, blk[m2]), fj);
+            term += spin(base, j) * (Jx[j] + 0.5 * fj);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+          if (lane < 4) hb[16 + lane] = lane == 0 ? term : 0.0;
+        }
       } else if (wq == 0) {
         if (lane < KA) {
           double a = gJx[lane];
