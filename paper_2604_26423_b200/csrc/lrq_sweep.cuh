@@ -175,7 +175,7 @@ struct SweepParams {
   int remap;
   int rbits;
   void* rdst[8];
-  int wd_prefetch;  // warp-decoupled sweeps: L2 prefetch of the next tile at each refill
+  int wd_prefetch;  // warp-decoupled sweeps: L2 prefetch of the tile this many ahead at each refill (0: off)
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }

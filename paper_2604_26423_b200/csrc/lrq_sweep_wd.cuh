@@ -356,9 +356,11 @@ __global__ void __launch_bounds__(TEAMS * kWdWarps * 32, 1) sweep_wd_kernel(cons
       const int c1 = (int)((uint64_t)tid & ((1ull << bl) - 1ull)), c4 = (int)((uint64_t)tid >> bl);
       tma_load_5d(dst, &P.tmap, fb, 0, 0, c1, 0, c4);
       // the next tile this CTA will load (fed by the other team about half a
-      // tile later) starts its trip to L2 now: that load then hits L2
+      // tile later) starts its trip to L2 now: that load then hits L2.
+      // ($LRQ_WD_PREFETCH = distance in tiles; 1 measured best, 2-4 slower:
+      // complex128 F 55.5 / 56.4 / 57.3 / 63.7 ms at n=33)
       if (P.wd_prefetch) {
-        const long long nx = tid + gridDim.x;
+        const long long nx = tid + (long long)P.wd_prefetch * gridDim.x;
         if (nx < P.num_tiles)
           tma_prefetch_5d(&P.tmap, 0, 0, (int)((uint64_t)nx & ((1ull << bl) - 1ull)), 0, (int)((uint64_t)nx >> bl));
       }
