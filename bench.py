@@ -765,7 +765,13 @@ def main():
         out = run_reference(args, rank, world)
     else:
         dist = init_dist(world)
-        out = (run_ours_dist if world > 1 else run_ours)(args, rank, world, local_rank, dist)
+        try:
+            out = (run_ours_dist if world > 1 else run_ours)(args, rank, world, local_rank, dist)
+        except Exception as exc:  # one parsable line saying what failed, then a failing exit
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "n_gpus": world, "error": f"{type(exc).__name__}: {exc}"}),
+                      flush=True)
+            raise
         if dist is not None:
             dist.destroy_process_group()
     if out is not None:
