@@ -3,6 +3,8 @@
 the builds over several processes so clock drift hits both alike.
 
     python scripts/ab_sweeps.py OLD.so NEW.so [n p prec rounds]
+
+A build may carry environment settings: "lib.so|LRQ_WD_QUARTER=0".
 """
 import json
 import os
@@ -40,9 +42,14 @@ print(json.dumps(out))
 
 
 def run(lib, n, p, prec):
+    # "path|KEY=VAL|KEY2=VAL2": the build plus environment settings
+    lib, *assigns = lib.split("|")
     env = dict(os.environ, LRQ_LIB=lib)
+    env.update(a.split("=", 1) for a in assigns)
     code = CHILD % (ROOT, ROOT, n, p, prec)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(f"{lib} {assigns}: {r.stderr[-800:]}")
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
