@@ -303,6 +303,15 @@ class DeviceState:
             raise StateError("device state has been released")
         return self._h
 
+    def _call(self, rc_fn) -> None:
+        """check(rc_fn()), retried once after draining the pool on an
+        out-of-memory error -- except for distributed / shard states, whose
+        calls are collective (a retry on one rank would desynchronise them)."""
+        if getattr(self, "_dist", False):
+            check(rc_fn())
+        else:
+            _retry_capacity(rc_fn)
+
     def _close(self, park: bool = True) -> None:
         """Release the state; the allocation is parked for reuse unless the
         pool already holds one for this shape (or park=False)."""
@@ -329,7 +338,7 @@ class DeviceState:
     def run(self, phase: np.ndarray, mixer: np.ndarray) -> None:
         phase = np.ascontiguousarray(phase, dtype=np.float64)
         mixer = np.ascontiguousarray(mixer, dtype=np.float64)
-        _retry_capacity(lambda: lib().lrq_run(self.handle, int(mixer.size), ptr(phase), ptr(mixer)))
+        self._call(lambda: lib().lrq_run(self.handle, int(mixer.size), ptr(phase), ptr(mixer)))
 
     def run_fields(self, phase: np.ndarray, field: np.ndarray, constant: np.ndarray, mixer: np.ndarray) -> None:
         """run() with per-layer single-Z fields (p x n) and constant phases (p)."""
@@ -340,13 +349,13 @@ class DeviceState:
         p = int(mixer.size)
         if field.size != p * self.n or constant.size != p:
             raise ValidationError(f"fields need shape ({p}, {self.n}) and constants ({p},)")
-        _retry_capacity(lambda: lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
+        self._call(lambda: lib().lrq_run_fields(self.handle, p, ptr(phase), ptr(field), ptr(constant), ptr(mixer)))
 
     def run_ex(self, phase: np.ndarray, mixer_q: np.ndarray) -> None:
         """run() with per-qubit mixer half-angles (p, n), equal up to sign per layer."""
         phase = np.ascontiguousarray(phase, dtype=np.float64)
         mixer_q = np.ascontiguousarray(mixer_q, dtype=np.float64)
-        _retry_capacity(lambda: lib().lrq_run_ex(self.handle, int(mixer_q.shape[0]), ptr(phase), ptr(mixer_q)))
+        self._call(lambda: lib().lrq_run_ex(self.handle, int(mixer_q.shape[0]), ptr(phase), ptr(mixer_q)))
 
     def permute_xor(self, mask: int) -> None:
         check(lib().lrq_permute_xor(self.handle, int(mask)))
@@ -355,11 +364,11 @@ class DeviceState:
         check(lib().lrq_reset(self.handle, int(which)))
 
     def apply_gate(self, kind: int, q0: int, q1: int = 0, theta: float = 0.0) -> None:
-        _retry_capacity(lambda: lib().lrq_apply_gate(self.handle, int(kind), int(q0), int(q1), float(theta)))
+        check(lib().lrq_apply_gate(self.handle, int(kind), int(q0), int(q1), float(theta)))
 
     def reduce(self) -> Reduction:
         r = Reduction()
-        _retry_capacity(lambda: lib().lrq_reduce(self.handle, ctypes.byref(r)))
+        self._call(lambda: lib().lrq_reduce(self.handle, ctypes.byref(r)))
         return r
 
     def recompute(self) -> None:
@@ -368,7 +377,7 @@ class DeviceState:
     def sample(self, u: np.ndarray) -> np.ndarray:
         u = np.ascontiguousarray(u, dtype=np.float64)
         out = np.empty(u.size, dtype=np.uint64)
-        _retry_capacity(lambda: lib().lrq_sample(self.handle, ptr(u), u.size, ptr(out)))
+        self._call(lambda: lib().lrq_sample(self.handle, ptr(u), u.size, ptr(out)))
         return out
 
     def copy_amps(self, start: int = 0, count: int | None = None) -> np.ndarray:
@@ -400,7 +409,7 @@ class DeviceState:
 
     def set_histogram(self, bins: int, lo: float = 0.0, hi: float = 1.0) -> None:
         """p-weighted E histogram of the next reducing pass (bins = 0: off)."""
-        _retry_capacity(lambda: lib().lrq_set_histogram(self.handle, int(bins), float(lo), float(hi)))
+        self._call(lambda: lib().lrq_set_histogram(self.handle, int(bins), float(lo), float(hi)))
         self.hist_bins = int(bins)
 
     def histogram(self) -> np.ndarray:
