@@ -87,7 +87,9 @@ int lrq_permute_xor(lrq_state *s, uint64_t mask);
 /* Gate-by-gate execution (engine.py:99-195) for circuits of any other shape:
  * reset to |0...0> (which = 0) or to the uniform state 2^(-n/2) (which = 1,
  * init_plus_state), then apply H (kind 0), RX(theta) (1) or RZZ(theta) (2)
- * one full pass at a time, with the reference kernels' complex arithmetic.
+ * one full pass at a time, with the reference kernels' complex arithmetic,
+ * or a Pauli X (3), Y (4), Z (5) on q0 (exact; the noisy engine's Pauli
+ * insertions, noise.py:70-98).
  * Asynchronous on the engine stream; lrq_recompute / lrq_sample after.     */
 int lrq_reset(lrq_state *s, int which);
 int lrq_apply_gate(lrq_state *s, int kind, int q0, int q1, double theta);

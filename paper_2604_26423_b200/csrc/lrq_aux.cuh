@@ -351,6 +351,18 @@ __global__ void gate1q_kernel(void* amps_, int n, int q, int kind, T c, T s) {
       u.y = mul_rn(add_rn(x.y, y.y), c);
       w.x = mul_rn(add_rn(x.x, -y.x), c);
       w.y = mul_rn(add_rn(x.y, -y.y), c);
+    } else if (kind == 3) {  // X: swap
+      u = y;
+      w = x;
+    } else if (kind == 4) {  // Y: (-i y, i x)
+      u.x = y.y;
+      u.y = -y.x;
+      w.x = -x.y;
+      w.y = x.x;
+    } else if (kind == 5) {  // Z: (x, -y)
+      u = x;
+      w.x = -y.x;
+      w.y = -y.y;
     } else {  // c x + (-i s) y, (-i s) x + c y with s = sin(theta / 2)
       u.x = add_rn(mul_rn(c, x.x), mul_rn(s, y.y));
       u.y = add_rn(mul_rn(c, x.y), -mul_rn(s, y.x));

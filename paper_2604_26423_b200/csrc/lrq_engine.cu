@@ -2092,8 +2092,8 @@ int lrq_apply_gate(lrq_state* s, int kind, int q0, int q1, double theta) {
   if (q0 < 0 || q0 >= n || (kind == 2 && (q1 < 0 || q1 >= n)))
     return fail(LRQ_EVALIDATION, "qubit out of range for " + std::to_string(n) + " qubits");
   if (kind == 2 && q0 == q1) return fail(LRQ_EVALIDATION, "RZZ qubits must differ");
-  if (kind < 0 || kind > 2) return fail(LRQ_EVALIDATION, "gate kind: 0 H, 1 RX, 2 RZZ");
-  if (kind != 0 && !isfinite(theta)) return fail(LRQ_EVALIDATION, "gate angle is not finite");
+  if (kind < 0 || kind > 5) return fail(LRQ_EVALIDATION, "gate kind: 0 H, 1 RX, 2 RZZ, 3 X, 4 Y, 5 Z");
+  if ((kind == 1 || kind == 2) && !isfinite(theta)) return fail(LRQ_EVALIDATION, "gate angle is not finite");
   DeviceGuard guard(s->device);
   const int grid = 4 * sm_count(s->device);
   const bool f32 = s->pbytes == 8;

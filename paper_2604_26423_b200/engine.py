@@ -266,23 +266,32 @@ def _apply_gate_kernel(amps: np.ndarray, gate, qubits: tuple) -> None:
     gate kernels as apply_gate), and the result is written back in place.
     Callers that own device states use apply_gate instead; this keeps code
     written against the reference's raw-array kernels working."""
+    if gate.kind not in _GATE_KIND:
+        raise ValidationError(f"unknown gate kind {gate.kind!r}")
+    q1 = qubits[1] if len(qubits) > 1 else 0
+    _seam_apply(amps, [(_GATE_KIND[gate.kind], qubits[0], q1, gate.theta or 0.0)], qubits)
+
+
+def _seam_apply(amps: np.ndarray, ops, qubits) -> None:
+    """Host-array seam: upload, run `ops` ((kind, q0, q1, theta): lrq_apply_gate
+    kinds 0 H, 1 RX, 2 RZZ, 3 X, 4 Y, 5 Z) as device passes, write back in place."""
     if amps.dtype not in (np.complex64, np.complex128) or amps.ndim != 1:
         raise ValidationError("the gate seam works on a flat complex64/complex128 array")
     n = amps.size.bit_length() - 1
     if amps.size != 1 << n:
         raise ValidationError(f"{amps.size} amplitudes do not form a state vector")
-    if gate.kind not in _GATE_KIND:
-        raise ValidationError(f"unknown gate kind {gate.kind!r}")
     for q in qubits:
         if not 0 <= q < n:
             raise ValidationError(f"qubit {q} out of range for {n} qubits")
+    if not ops:
+        return
     pb = amps.dtype.itemsize
     dev = _SEAM.get((n, pb))
     if dev is None:
         dev = _SEAM[(n, pb)] = _native.DeviceState(n, pb)
     dev.store_amps(amps)
-    q1 = qubits[1] if len(qubits) > 1 else 0
-    dev.apply_gate(_GATE_KIND[gate.kind], qubits[0], q1, gate.theta or 0.0)
+    for kind, q0, q1, theta in ops:
+        dev.apply_gate(kind, q0, q1, theta)
     amps[...] = dev.copy_amps()
 
 

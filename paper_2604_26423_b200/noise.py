@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _native
 from .circuit import CircuitIR, complete_edge_pairs
-from .engine import Precision, ShotSet, check_memory, expected_r_from_probs
+from .engine import Precision, ShotSet, _seam_apply, check_memory, expected_r_from_probs
 from .errors import FitError, ValidationError
 from .problem import WmcInstance
 from .rng import derive_rng
@@ -161,6 +161,35 @@ def batch_programs(circuit: CircuitIR, cfg: DepolarizingConfig):
             mixer[:, li, q] = np.where(z[:, q], -half, half)
     xmask = (x.astype(np.uint64) << np.arange(n, dtype=np.uint64)[None, :]).sum(axis=1).astype(np.uint32)
     return phase, mixer, xmask
+
+
+# The reference's host Pauli kernels (noise.py:70-98), in place on a flat
+# complex array, kept as the same private seam: each runs on the GPU as one
+# exact pass (lrq_apply_gate kinds 3 X, 4 Y, 5 Z).  The batched trajectory
+# engine below does not use them: it propagates Pauli frames on the host.
+_PAULI_KIND = (None, 3, 4, 5)
+
+
+def _x_kernel(amps: np.ndarray, q: int) -> None:
+    _seam_apply(amps, [(3, q, 0, 0.0)], (q,))
+
+
+def _y_kernel(amps: np.ndarray, q: int) -> None:
+    _seam_apply(amps, [(4, q, 0, 0.0)], (q,))
+
+
+def _z_kernel(amps: np.ndarray, q: int) -> None:
+    _seam_apply(amps, [(5, q, 0, 0.0)], (q,))
+
+
+def _apply_pauli_pair(amps: np.ndarray, code: int, qa: int, qb: int) -> None:
+    """The two-qubit Pauli numbered 1..15 (base-4 digits a, b; 0 = I, 1 X,
+    2 Y, 3 Z) on qubits (qa, qb), in one upload."""
+    if not 0 < int(code) < 16:
+        raise ValidationError(f"two-qubit Pauli code must be 1..15, got {code}")
+    pa, pb = divmod(int(code), 4)
+    ops = [(_PAULI_KIND[k], q, 0, 0.0) for k, q in ((pa, qa), (pb, qb)) if k]
+    _seam_apply(amps, ops, (qa, qb))
 
 
 def _tile_bits(precision: Precision) -> int:
