@@ -81,3 +81,39 @@ def test_lqsv_load_of_reference_dump_and_round_trip(tmp_path, name, n, seed, p, 
     # the loaded state is a live device state: reductions and sampling work on it
     inst = L.solve_instance(L.generate_instance(n, seed))
     assert L.exact_expected_r(ref, inst) == pytest.approx(L.exact_expected_r(mine, inst), rel=1e-5)
+
+
+@pytest.mark.parametrize("n", [3, 14])
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_pauli_seams_are_exact(n, dtype):
+    """noise._x/_y/_z_kernel and _apply_pauli_pair (the reference's private
+    Pauli seams, noise.py:70-98) on the GPU: exact, in place on the host array."""
+    from paper_2604_26423_b200 import noise
+
+    rng = np.random.default_rng(n)
+    start = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)).astype(dtype)
+    z = np.arange(1 << n)
+
+    def pauli(a, k, q):  # numpy restatement by index: X swaps, Y = i X Z, Z flips the sign of bit 1
+        bit = (z >> q) & 1
+        if k == 1:
+            return a[z ^ (1 << q)]
+        if k == 2:
+            return np.where(bit == 1, 1j, -1j).astype(a.dtype) * a[z ^ (1 << q)]
+        return np.where(bit == 1, -1, 1).astype(a.dtype) * a
+
+    for k, fn in ((1, noise._x_kernel), (2, noise._y_kernel), (3, noise._z_kernel)):
+        for q in (0, n - 1):
+            amps = start.copy()
+            fn(amps, q)
+            np.testing.assert_array_equal(amps, pauli(start, k, q))
+    for code in range(1, 16):
+        amps = start.copy()
+        noise._apply_pauli_pair(amps, code, 0, n - 1)
+        pa, pb = divmod(code, 4)
+        want = start
+        if pb:
+            want = pauli(want, pb, n - 1)
+        if pa:
+            want = pauli(want, pa, 0)
+        np.testing.assert_array_equal(amps, want)
