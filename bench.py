@@ -490,6 +490,33 @@ def extra_config(L, _native, cfg, steps, peak):
             "sum_p": red.sum_p, "max_cut_E": red.min_energy}
 
 
+def sample_check(L, circ, solved, prec, shots=10000, groups=40):
+    """Untimed: chi-square of `shots` samples of the run's state against the
+    exact distribution of C (the device histogram pass), grouped into ~40
+    equiprobable bins (north_star: sampled histograms must pass chi-square)."""
+    from scipy import stats
+
+    sv = L.run_circuit(circ, prec, memory_budget=BUDGET)
+    try:
+        d = L.exact_cut_distribution(sv, solved, bins=2048)
+        shot_set = L.sample(sv, shots, 3)
+    finally:
+        sv.release()
+    p = d.probs / d.probs.sum()
+    gid = np.minimum((np.cumsum(p) * groups).astype(int), groups - 1)
+    exp_g = np.bincount(gid, weights=p, minlength=groups) * shots
+    obs_g = np.bincount(gid[d.bin_of(L.cut_values(solved, shot_set.indices))], minlength=groups).astype(float)
+    keep = exp_g > 5
+    chi2 = float(np.sum((obs_g[keep] - exp_g[keep]) ** 2 / exp_g[keep]))
+    df = int(keep.sum()) - 1
+    other_o, other_e = obs_g[~keep].sum(), exp_g[~keep].sum()
+    if other_e > 5:
+        chi2 += (other_o - other_e) ** 2 / other_e
+        df += 1
+    return {"shots": shots, "bins": int(df + 1), "chi2": chi2, "df": df, "p_value": float(stats.chi2.sf(chi2, df)),
+            "source": "exact C histogram from the device pass (lrq_set_histogram), 2048 fine bins grouped ~equiprobable"}
+
+
 def run_ours(args, rank, world, local_rank, dist):
     os.environ.setdefault("LRQ_DEVICE", str(local_rank))
     import paper_2604_26423_b200 as L
@@ -546,6 +573,7 @@ def run_ours(args, rank, world, local_rank, dist):
         del sv
     e2e_s_max = max_over_ranks(dist, time.perf_counter() - t0)
     r_sampled = L.approximation_ratio(solved, shots_set)
+    chi = sample_check(L, circ, solved, prec)  # untimed: 10k shots against the exact C distribution
     _native.drain_pool()
 
     extra = {}
@@ -603,7 +631,8 @@ def run_ours(args, rank, world, local_rank, dist):
         "configs": extra,
         "results": {"exact_r": r_exact, "sampled_r": r_sampled, "sum_p": red.sum_p,
                     "max_cut": solved.optimal_cut.value,
-                    "min_cut": 0.5 * (inst.total_weight() - srch.max_energy)},
+                    "min_cut": 0.5 * (inst.total_weight() - srch.max_energy),
+                    "chi_square": chi},
     }
 
 
