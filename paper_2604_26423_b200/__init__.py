@@ -25,6 +25,7 @@ from .engine import (
     CutDistribution,
     Precision,
     draw_indices,
+    drain_state_pool,
     exact_cut_distribution,
     apply_gate,
     apply_h,

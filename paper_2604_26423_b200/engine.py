@@ -58,6 +58,15 @@ class Precision(enum.Enum):
         return self.dtype.itemsize
 
 
+def drain_state_pool() -> None:
+    """Free the HBM of dropped states kept for reuse.  A dropped StateVector's
+    allocation is parked for the next state of the same shape (no cudaMalloc
+    per run_circuit); this library's own allocations drain the pool when they
+    run out, other code that needs the memory calls this first.
+    StateVector.release() frees a state at once."""
+    _native.drain_pool()
+
+
 def state_bytes(num_qubits: int, precision: Precision) -> int:
     return precision.bytes_per_amplitude << num_qubits
 
