@@ -235,24 +235,20 @@ def sweep_labels(n_local, B, p, world):
 
 def per_kernel(ms, kinds, labels, n_local, B, peak, steps):
     """Group the sweep records of `steps` runs by label: mean ms, bytes, GB/s,
-    fraction of peak, share of the sweeps' time."""
+    fraction of peak, share of the sweeps' time.  Records other than sweeps
+    (remaps, flips, the finalize) are skipped; sweeps map onto `labels` (one
+    run's plan) in order."""
     recs = {}
-    i = 0
-    per_run = [k for k in kinds]
-    # records per run: sweeps (PMFRQ) in plan order plus remap/flip/finalize records
     j = 0
-    for m, k in zip(ms, per_run):
+    for m, k in zip(ms, kinds):
         if k in "PMFRQ":
             lab, kern = labels[j % len(labels)]
             j += 1
             recs.setdefault(lab, {"kernel": kern, "ms": []})["ms"].append(m)
-        i += 1
     total = sum(sum(r["ms"]) for r in recs.values()) or 1.0
     out = {}
     for lab, r in recs.items():
-        r["bytes"] = (1 if lab.startswith("P") or lab.startswith("Q") else 2) * (B << n_local)
-    for lab, r in recs.items():
-        byts = (1 if lab.startswith("P") or lab.startswith("Q") else 2) * (B << n_local)
+        byts = (1 if lab.startswith("P") or lab.startswith("Q") else 2) * (B << n_local)  # P writes, Q reads only
         avg = statistics.mean(r["ms"])
         gbs = byts / (avg * 1e-3) / 1e9
         out[lab] = {"kernel": r["kernel"], "launches_per_step": len(r["ms"]) // max(1, steps), "ms_avg": round(avg, 4),

@@ -34,3 +34,42 @@ def test_kernel_launch_accounting():
     assert bench.kernel_launches("PMYFMTQZ", 24) == 6
     assert bench.kernel_launches("PMFMRXZ", 24) == 8
     assert bench.kernel_launches("PMFMRZ", 32) == 5 + 3  # multi-CTA finalize from 8192 tiles
+
+
+def test_workloads_follow_the_baseline_configs():
+    import argparse
+
+    import bench
+
+    def wl(world, **kw):
+        a = argparse.Namespace(config=0, n=0, p=0, precision="", shots=0)
+        for k, v in kw.items():
+            setattr(a, k, v)
+        return bench.workload(a, world)
+
+    assert wl(1)[:4] == (32, 10, "fp32", 1000)          # configs[2]: the metric's config
+    assert wl(2)[:4] == (34, 3, "fp64", 10000)          # configs[3] over 2 GPUs
+    assert wl(8)[:4] == (36, 3, "fp64", 10000)          # configs[4]: the north-star target
+    assert wl(1, config=4)[:4] == (33, 3, "fp64", 10000)  # largest one-GPU point of configs[3]
+    assert wl(1, config=2)[:4] == (26, 3, "fp64", 1000)
+    assert wl(8)[5] == "weak"                            # 2^33 amplitudes per GPU at every N
+    assert wl(8, config=4)[5] == "strong" and wl(2, config=4)[5] == "strong"  # n=34 fixed
+
+
+def test_per_kernel_roofline_accounting():
+    import bench
+
+    labels = [("P(H4)", "sweep_wd_kernel"), ("M(A)", "sweep_kernel"), ("F(H)", "sweep_wd_kernel"),
+              ("R(A)", "sweep_kernel")]
+    # two runs: sweeps plus a finalize record 'Z' each
+    ms = [9.0, 11.0, 20.0, 17.0, 0.1, 9.0, 11.0, 20.0, 17.0, 0.1]
+    kinds = "PMFRZPMFRZ"
+    pk = bench.per_kernel(ms, kinds, labels, 32, 8, 6553.3, 2)
+    st = 8 << 32
+    assert pk["P(H4)"]["bytes_per_launch"] == st and pk["M(A)"]["bytes_per_launch"] == 2 * st
+    assert pk["F(H)"]["launches_per_step"] == 1
+    assert abs(pk["M(A)"]["achieved_GBps"] - 2 * st / 11e-3 / 1e9) < 0.1
+    assert abs(sum(v["time_share"] for v in pk.values()) - 1.0) < 1e-3
+    k, d = bench.dominant(pk, 6553.3)
+    assert k == "sweep_wd_kernel" and d["labels"] == ["F(H)", "P(H4)"]
+    assert abs(d["achieved"] - 3 * st / 29e-3 / 1e9) < 0.1  # (P bytes + F bytes) / (9 + 20 ms)
