@@ -543,8 +543,8 @@ def noisy_batch(n: int, precision_bytes: int, phase: np.ndarray, mixer: np.ndarr
     if shots:
         u = np.ascontiguousarray(u, dtype=np.float64)
         idx = np.empty((T, shots), dtype=np.uint64)
-    _retry_capacity(lambda: lib().lrq_noisy_batch(n, precision_bytes, dev, T, p, ptr(phase), ptr(mixer), ptr(xmask), shots,
-                                ptr(u) if shots else None, ptr(probs) if probs is not None else None,
-                                ptr(idx) if idx is not None else None))
+    _retry_capacity(lambda: lib().lrq_noisy_batch(
+        n, precision_bytes, dev, T, p, ptr(phase), ptr(mixer), ptr(xmask), shots, ptr(u) if shots else None,
+        ptr(probs) if probs is not None else None, ptr(idx) if idx is not None else None))
     return probs, idx
 
