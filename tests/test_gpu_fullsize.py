@@ -80,3 +80,22 @@ def test_full_size_distributed_plan_matches_dense():
     for shots in (shots_sh, shots_de):
         ratios = L.shot_ratios(inst, shots)
         assert abs(ratios.mean() - r_de) < 4 * ratios.std() / math.sqrt(len(ratios))
+
+
+def test_largest_one_gpu_complex64_state():
+    """n=34 complex64 (128 GiB, 2^21 tiles): the largest complex64 state one
+    B200 holds.  Norm, the fused max-cut search against the exhaustive one's
+    C*, and sampled r within 4 SE of the exact r."""
+    n, p = 34, 2
+    inst = L.solve_instance(L.generate_instance(n, 1), limit=n)
+    sv = L.run_circuit(L.build_circuit(L.generate_instance(n, 1), L.LrQaoaParams(p=p)), "fp32", BUDGET)
+    try:
+        red = sv.device_state.reduce()
+        assert abs(red.sum_p - 1.0) < 1e-5
+        assert float(L.cut_values(inst, [red.argmax_cut])[0]) == inst.optimal_cut.value
+        r = L.exact_expected_r(sv, inst)
+        ratios = L.shot_ratios(inst, L.sample(sv, 4000, rng_seed=2))
+        assert abs(ratios.mean() - r) < 4 * ratios.std() / math.sqrt(len(ratios))
+    finally:
+        sv.release()
+        _native.drain_pool()
